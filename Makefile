@@ -1,0 +1,32 @@
+# Builds the in-tree C-ABI library paper_2504_07042_b200/_lib/libhx_axlocal.so
+# for sm_100a, plus the C oracle helpers.  `make -j` compiles the per-order
+# generic kernel objects in parallel.
+NVCC      ?= nvcc
+ARCH      ?= -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   ?= -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $(ARCH)
+SRC       := paper_2504_07042_b200/csrc
+OBJ       := build/obj
+LIB       := paper_2504_07042_b200/_lib/libhx_axlocal.so
+ORDERS    := 2 3 4 5 6 7 8 9 10 11 12 13 14 15 16
+GEN_OBJS  := $(foreach n,$(ORDERS),$(OBJ)/ax_generic_$(n).o)
+OBJS      := $(GEN_OBJS) $(OBJ)/ax_fast.o $(OBJ)/setup.o $(OBJ)/capi.o
+HEADERS   := $(SRC)/hx_common.cuh include/hx_axlocal.h $(wildcard $(SRC)/*.cuh)
+
+all: $(LIB)
+
+$(OBJ):
+	mkdir -p $(OBJ) paper_2504_07042_b200/_lib
+
+$(OBJ)/ax_generic_%.o: $(SRC)/ax_generic.cu $(HEADERS) | $(OBJ)
+	$(NVCC) $(NVFLAGS) -DHX_N1=$* -c $< -o $@
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HEADERS) | $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

@@ -1,0 +1,159 @@
+/*
+ * hx_axlocal.h — C ABI of the B200-native AxLocal (CEED BK5) library.
+ *
+ * Drop-in boundary for the reference's element-local operator
+ * (hosfem, pkg/src/hosfem/axlocal.py).  The reference is a Python class API,
+ * not an FFI; each entry point below replaces one piece of it and is bound
+ * from Python with ctypes (see INTEGRATION.md for the stub).
+ *
+ * Conventions (all match the reference):
+ *   - fp64 everywhere; node (i,j,k) of an element is flat i + j*n1 + k*n1*n1;
+ *   - fields x, y are (E, n1^3, n_col) row-major, n_col innermost
+ *     (LocalField, mesh.py:140-155);
+ *   - vertices are (E, 8, 3), vertex b at reference corner bits (r,s,t);
+ *   - stored factors are SoA (E, 6, n1^3) in the order g00 g01 g02 g11 g12 g22
+ *     (the reference keeps AoS (E, n1^3, 6), geometry.py:264-275);
+ *   - every pointer in an hx_* call is a DEVICE pointer owned by the caller
+ *     (torch), except hx_set_basis's host arrays; nothing here allocates;
+ *   - calls are stream-ordered on the given cudaStream_t (passed as void*),
+ *     and never synchronise except where documented;
+ *   - no C++ exception crosses this boundary; every call returns an hx_status
+ *     and hx_last_error() describes the last failure on the calling thread.
+ */
+#ifndef HX_AXLOCAL_H
+#define HX_AXLOCAL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HX_OK = 0,
+  HX_ERR_INVALID = 1,     /* maps to ValueError (axlocal.py:68-81, 123-127, 238-243) */
+  HX_ERR_GEOMETRY = 2,    /* maps to GeometryError (geometry.py:64-65, 243-247, 344-346) */
+  HX_ERR_CUDA = 3,        /* launch / runtime failure */
+  HX_ERR_UNSUPPORTED = 4  /* order outside 1..15 etc. */
+} hx_status;
+
+/* Equation (axlocal.py:45-47). */
+typedef enum { HX_POISSON = 0, HX_HELMHOLTZ = 1 } hx_equation;
+
+/* FactorSource (axlocal.py:50-55). */
+typedef enum {
+  HX_STORED = 0,
+  HX_TRILINEAR = 1,
+  HX_TRILINEAR_MERGED = 2,
+  HX_TRILINEAR_PARTIAL = 3,
+  HX_PARALLELEPIPED = 4
+} hx_factor_source;
+
+/*
+ * Arguments of one apply.  Replaces LocalOperator.apply/_apply_range/_factor_stage
+ * (axlocal.py:171-258): y = A x for all E elements of the operator.
+ * Which factor pointers must be non-NULL depends on (equation, source):
+ *   STORED              g (E,6,n1^3) SoA;  Helmholtz: gwj (E,n1^3)
+ *   TRILINEAR           verts (E,8,3)
+ *   TRILINEAR_PARTIAL   verts, lam_geo (E,n1^3)       [Poisson only]
+ *   TRILINEAR_MERGED    verts, lam2, lam3 (E,n1^3)    [Helmholtz only]
+ *   PARALLELEPIPED      h (E,7)
+ * Helmholtz coefficients (all but MERGED): lam0 / lam1 (E,n1^3) device fields,
+ * or NULL to use the scalar lam0_value / lam1_value for every node
+ * (_coeff_field, axlocal.py:88-101; None means 1).
+ */
+typedef struct {
+  int32_t order;          /* N, 1..15 */
+  int32_t n_col;          /* 1 or 3 */
+  int32_t equation;       /* hx_equation */
+  int32_t factor_source;  /* hx_factor_source */
+  int64_t n_elements;     /* E >= 0 (0 is a no-op) */
+  const double* x;
+  double* y;
+  const double* verts;
+  const double* h;
+  const double* g;
+  const double* gwj;
+  const double* lam_geo;
+  const double* lam2;
+  const double* lam3;
+  const double* lam0;
+  const double* lam1;
+  double lam0_value;
+  double lam1_value;
+  int32_t kernel;         /* 0 = best available; 1 = generic slice kernel (test hook) */
+  int32_t reserved;
+} hx_axlocal_args;
+
+/* Library version string. */
+const char* hx_version(void);
+
+/* Human-readable description of the last error on this thread ("" if none). */
+const char* hx_last_error(void);
+
+/*
+ * Upload the GLL basis of one order to the current device's __constant__ bank.
+ * points (n1), weights (n1), dmat (n1*n1 row-major, [i][j] = l_j'(x_i)) are HOST
+ * arrays from SpectralBasis.build (basis.py:110-136).  Synchronous.  Must be
+ * called once per (device, order) before any other call with that order.
+ */
+int hx_set_basis(int32_t order, const double* points, const double* weights, const double* dmat);
+
+/* y = A x.  Replaces LocalOperator.apply (axlocal.py:235-258). */
+int hx_axlocal(const hx_axlocal_args* args, void* stream);
+
+/*
+ * Degenerate-geometry check of the trilinear route over all GLL nodes
+ * (trilinear_factors(validate=True), geometry.py:342-346, run once in
+ * LocalOperator.__init__, axlocal.py:156).  Writes into *first_bad_out (device,
+ * int64) the smallest flat index e*n1^3 + node with det(8J) <= 0, or INT64_MAX
+ * when every node is valid.  The call initialises *first_bad_out itself
+ * (stream-ordered); the caller reads it back after the stream reaches it.
+ */
+int hx_trilinear_validate(int32_t order, int64_t n_elements, const double* verts,
+                          int64_t* first_bad_out, void* stream);
+
+/* lam_geo = 0.125 w / det(8J) per node (partial_recompute_setup, geometry.py:414-424). */
+int hx_setup_partial(int32_t order, int64_t n_elements, const double* verts, double* lam_geo_out,
+                     void* stream);
+
+/*
+ * lam2 = lam_geo * lam0, lam3 = (lam_geo * det(8J)^2/64) * lam1
+ * (merged_scalar_setup, geometry.py:401-411, as called at axlocal.py:159-165).
+ * lam0/lam1 may be NULL to use the scalar values.
+ */
+int hx_setup_merged(int32_t order, int64_t n_elements, const double* verts, const double* lam0,
+                    double lam0_value, const double* lam1, double lam1_value, double* lam2_out,
+                    double* lam3_out, void* stream);
+
+/*
+ * Stored (Nek-style) factors through the general route: nodal coordinates of
+ * the trilinear map, collocation Jacobian by D contractions, w|J| J^-1 J^-T
+ * (element_node_coords + discrete_jacobians + factors_from_jacobians,
+ * mesh.py:130-137, geometry.py:225-276).  g_out SoA (E,6,n1^3); gwj_out
+ * (E,n1^3) may be NULL.  *first_bad_out as in hx_trilinear_validate.
+ */
+int hx_setup_stored(int32_t order, int64_t n_elements, const double* verts, double* g_out,
+                    double* gwj_out, int64_t* first_bad_out, void* stream);
+
+/*
+ * Parallelepiped constants h (E,7) = (det J^-1 J^-T sym6, det) with
+ * J = (v1-v0 | v2-v0 | v4-v0)/2 (parallelepiped_setup, geometry.py:362-380).
+ * *bad_out (device int64) receives 2*e + 0 for the smallest element e whose
+ * vertices fail the parallelepiped identities (defect > 1e-10 * scale), or
+ * 2*e + 1 when its det <= 0 (whichever e is smaller), else INT64_MAX.
+ */
+int hx_setup_parallelepiped(int64_t n_elements, const double* verts, double* h_out, int64_t* bad_out,
+                            void* stream);
+
+/*
+ * Element classification (make_element, mesh.py:97-107): kind_out[e] = 1 when
+ * the defect is <= 1e-12 * max(1, max|v|) (parallelepiped), else 0 (trilinear).
+ */
+int hx_classify_elements(int64_t n_elements, const double* verts, int8_t* kind_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HX_AXLOCAL_H */

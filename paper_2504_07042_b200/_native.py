@@ -1,0 +1,117 @@
+"""ctypes binding of the in-tree C-ABI library ``_lib/libhx_axlocal.so``.
+
+The library is the product: there is no CPU fallback.  Loading fails loudly
+when the shared object is missing (run ``make`` or ``__graft_entry__.build()``),
+and every call that returns a non-zero ``hx_status`` raises: HX_ERR_INVALID and
+HX_ERR_UNSUPPORTED as ``ValueError`` (like the reference's validation,
+axlocal.py:67-81), HX_ERR_CUDA as ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+__all__ = ["lib", "AxArgs", "check", "LIB_PATH", "SYMBOLS"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libhx_axlocal.so")
+
+#: Every entry point declared in include/hx_axlocal.h.
+SYMBOLS = (
+    "hx_version",
+    "hx_last_error",
+    "hx_set_basis",
+    "hx_axlocal",
+    "hx_trilinear_validate",
+    "hx_setup_partial",
+    "hx_setup_merged",
+    "hx_setup_stored",
+    "hx_setup_parallelepiped",
+    "hx_classify_elements",
+)
+
+HX_OK, HX_ERR_INVALID, HX_ERR_GEOMETRY, HX_ERR_CUDA, HX_ERR_UNSUPPORTED = range(5)
+
+_c_p = ctypes.c_void_p
+_i32, _i64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+
+class AxArgs(ctypes.Structure):
+    """Mirror of ``hx_axlocal_args`` (include/hx_axlocal.h)."""
+
+    _fields_ = [
+        ("order", _i32),
+        ("n_col", _i32),
+        ("equation", _i32),
+        ("factor_source", _i32),
+        ("n_elements", _i64),
+        ("x", _c_p),
+        ("y", _c_p),
+        ("verts", _c_p),
+        ("h", _c_p),
+        ("g", _c_p),
+        ("gwj", _c_p),
+        ("lam_geo", _c_p),
+        ("lam2", _c_p),
+        ("lam3", _c_p),
+        ("lam0", _c_p),
+        ("lam1", _c_p),
+        ("lam0_value", _f64),
+        ("lam1_value", _f64),
+        ("kernel", _i32),
+        ("reserved", _i32),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"CUDA library {LIB_PATH} is missing; build it with `make -j` (or __graft_entry__.build()). "
+            "There is no CPU fallback."
+        )
+    so = ctypes.CDLL(LIB_PATH)
+    so.hx_version.restype = ctypes.c_char_p
+    so.hx_version.argtypes = []
+    so.hx_last_error.restype = ctypes.c_char_p
+    so.hx_last_error.argtypes = []
+    so.hx_set_basis.restype = ctypes.c_int
+    so.hx_set_basis.argtypes = [_i32, _c_p, _c_p, _c_p]
+    so.hx_axlocal.restype = ctypes.c_int
+    so.hx_axlocal.argtypes = [ctypes.POINTER(AxArgs), _c_p]
+    so.hx_trilinear_validate.restype = ctypes.c_int
+    so.hx_trilinear_validate.argtypes = [_i32, _i64, _c_p, _c_p, _c_p]
+    so.hx_setup_partial.restype = ctypes.c_int
+    so.hx_setup_partial.argtypes = [_i32, _i64, _c_p, _c_p, _c_p]
+    so.hx_setup_merged.restype = ctypes.c_int
+    so.hx_setup_merged.argtypes = [_i32, _i64, _c_p, _c_p, _f64, _c_p, _f64, _c_p, _c_p, _c_p]
+    so.hx_setup_stored.restype = ctypes.c_int
+    so.hx_setup_stored.argtypes = [_i32, _i64, _c_p, _c_p, _c_p, _c_p, _c_p]
+    so.hx_setup_parallelepiped.restype = ctypes.c_int
+    so.hx_setup_parallelepiped.argtypes = [_i64, _c_p, _c_p, _c_p, _c_p]
+    so.hx_classify_elements.restype = ctypes.c_int
+    so.hx_classify_elements.argtypes = [_i64, _c_p, _c_p, _c_p]
+    return so
+
+
+def lib():
+    """The loaded library (loaded once per process)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                _lib = _load()
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == HX_OK:
+        return
+    msg = lib().hx_last_error().decode(errors="replace")
+    if status in (HX_ERR_INVALID, HX_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    raise RuntimeError(f"hx_axlocal library error {status}: {msg}")

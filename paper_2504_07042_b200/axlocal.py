@@ -1,0 +1,350 @@
+"""B200 AxLocal operator: drop-in for ``hosfem.axlocal`` (reference pkg/src/hosfem/axlocal.py).
+
+Same public surface — ``Equation``, ``FactorSource``, ``KernelSpec``,
+``LocalOperator(spec, elements, basis, lam0=None, lam1=None)`` with
+``.apply(x, threads=1)``, and ``ax_local_apply`` — with the same validation
+and error types (axlocal.py:67-81, 123-169, 238-243).  Setup and apply run as
+hand-written sm_100a kernels in ``_lib/libhx_axlocal.so`` (C ABI in
+``include/hx_axlocal.h``); there is no CPU fallback.
+
+Inputs beyond the reference's:
+* ``elements`` may also be a ``BoxMesh``, or an (E, 8, 3) fp64 array / torch
+  tensor of vertices (kinds then classified on the GPU with make_element's rule);
+* ``apply`` also takes an (E, n1^3, n_col) or (E, n1^3) fp64 CUDA tensor and then
+  returns a CUDA tensor (no host round trip); ``apply_(x, y)`` writes into a
+  preallocated output.  A host ``LocalField`` in gives a host ``LocalField`` out
+  (copied through pinned memory).
+``threads`` is accepted for signature compatibility and ignored: the element
+split is the CUDA grid, and results are bitwise independent of it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .mesh import BoxMesh, Element, ElementKind, LocalField
+
+__all__ = [
+    "Equation",
+    "FactorSource",
+    "KernelSpec",
+    "LocalOperator",
+    "ax_local_apply",
+    "GeometryError",
+]
+
+
+class GeometryError(ValueError):
+    """Degenerate or inconsistent element geometry (geometry.py:64-65)."""
+
+
+class Equation(enum.Enum):
+    POISSON = "poisson"
+    HELMHOLTZ = "helmholtz"
+
+
+class FactorSource(enum.Enum):
+    STORED = "stored"
+    TRILINEAR_RECOMPUTE = "trilinear"
+    TRILINEAR_MERGED = "trilinear-merged"
+    TRILINEAR_PARTIAL = "trilinear-partial"
+    PARALLELEPIPED_RECOMPUTE = "parallelepiped"
+
+
+_HX_SOURCE = {
+    FactorSource.STORED: 0,
+    FactorSource.TRILINEAR_RECOMPUTE: 1,
+    FactorSource.TRILINEAR_MERGED: 2,
+    FactorSource.TRILINEAR_PARTIAL: 3,
+    FactorSource.PARALLELEPIPED_RECOMPUTE: 4,
+}
+
+
+def _coerce_enum(cls, value):
+    if isinstance(value, cls):
+        return value
+    # accept the reference's own enum members (same values) and plain strings
+    return cls(getattr(value, "value", value))
+
+
+@dataclass(frozen=True)
+class KernelSpec:
+    """What to apply: equation, columns, factor variant, order (axlocal.py:58-85)."""
+
+    equation: Equation
+    n_col: int
+    factor_source: FactorSource
+    order: int
+
+    def __post_init__(self):
+        object.__setattr__(self, "equation", _coerce_enum(Equation, self.equation))
+        object.__setattr__(self, "factor_source", _coerce_enum(FactorSource, self.factor_source))
+        if self.n_col not in (1, 3):
+            raise ValueError("n_col must be 1 or 3")
+        if self.order < 1:
+            raise ValueError("order must be at least 1")
+        if self.factor_source is FactorSource.TRILINEAR_MERGED and self.equation is not Equation.HELMHOLTZ:
+            raise ValueError("the merged-scalar variant exists for Helmholtz only")
+        if self.factor_source is FactorSource.TRILINEAR_PARTIAL and self.equation is not Equation.POISSON:
+            raise ValueError("the partial-recompute variant exists for Poisson only")
+
+    @property
+    def n1(self) -> int:
+        return self.order + 1
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+_BASIS_UPLOADED: set = set()
+
+
+def _ensure_basis(device_index: int, basis) -> None:
+    key = (device_index, int(basis.order))
+    if key in _BASIS_UPLOADED:
+        return
+    torch = _torch()
+    pts = np.ascontiguousarray(basis.points, dtype=np.float64)
+    wts = np.ascontiguousarray(basis.weights, dtype=np.float64)
+    dm = np.ascontiguousarray(basis.diff_matrix, dtype=np.float64)
+    with torch.cuda.device(device_index):
+        _native.check(
+            _native.lib().hx_set_basis(
+                int(basis.order), pts.ctypes.data, wts.ctypes.data, dm.ctypes.data
+            )
+        )
+    _BASIS_UPLOADED.add(key)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device):
+    return ctypes.c_void_p(_torch().cuda.current_stream(device).cuda_stream)
+
+
+def _read_i64(t) -> int:
+    return int(t.item())
+
+
+class LocalOperator:
+    """Batched Y = A X over a fixed element set on one GPU (axlocal.py:107-258)."""
+
+    def __init__(self, spec: KernelSpec, elements, basis, lam0=None, lam1=None, device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("LocalOperator needs a CUDA device (B200); there is no CPU fallback")
+        if basis.order != spec.order:
+            raise ValueError("basis order does not match the kernel spec")
+        self.spec = spec
+        self.basis = basis
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        dev = self.device
+        n1 = basis.n1
+        n3 = n1**3
+        helm = spec.equation is Equation.HELMHOLTZ
+        if not helm and (lam0 is not None or lam1 is not None):
+            raise ValueError("coefficient fields apply to the Helmholtz operator only")
+
+        verts, kinds = self._vertices(elements, dev)
+        self.n_elements = int(verts.shape[0])
+        if self.n_elements == 0:
+            raise ValueError("need at least one element")
+        self._verts = verts
+        _ensure_basis(dev.index, basis)
+        source = spec.factor_source
+        E = self.n_elements
+        stream = _stream(dev)
+        L = _native.lib()
+        self._h = self._g = self._gwj = self._lam_geo = self._lam2 = self._lam3 = None
+
+        kinds = kinds if kinds is not None else self._classify(verts, stream)
+        if source is FactorSource.PARALLELEPIPED_RECOMPUTE:
+            if kinds - {ElementKind.PARALLELEPIPED}:
+                raise ValueError("parallelepiped recompute needs an all-parallelepiped element set")
+            self._h = torch.empty((E, 7), dtype=torch.float64, device=dev)
+            bad = torch.empty((1,), dtype=torch.int64, device=dev)
+            _native.check(L.hx_setup_parallelepiped(E, _ptr(verts), _ptr(self._h), _ptr(bad), stream))
+            b = _read_i64(bad)
+            if b != np.iinfo(np.int64).max:
+                if b % 2 == 0:
+                    raise GeometryError("vertices do not form a parallelepiped")
+                raise GeometryError("degenerate parallelepiped (det <= 0)")
+        elif source is FactorSource.STORED:
+            self._g = torch.empty((E, 6, n3), dtype=torch.float64, device=dev)
+            self._gwj = torch.empty((E, n3), dtype=torch.float64, device=dev) if helm else None
+            bad = torch.empty((1,), dtype=torch.int64, device=dev)
+            _native.check(
+                L.hx_setup_stored(spec.order, E, _ptr(verts), _ptr(self._g), _ptr(self._gwj), _ptr(bad), stream)
+            )
+            b = _read_i64(bad)
+            if b != np.iinfo(np.int64).max:
+                raise GeometryError(f"non-positive Jacobian determinant at element {b // n3}, node {b % n3}")
+        else:
+            if kinds - {ElementKind.TRILINEAR, ElementKind.PARALLELEPIPED}:
+                raise ValueError("trilinear recompute variants need trilinear elements")
+            bad = torch.empty((1,), dtype=torch.int64, device=dev)
+            _native.check(L.hx_trilinear_validate(spec.order, E, _ptr(verts), _ptr(bad), stream))
+            b = _read_i64(bad)
+            if b != np.iinfo(np.int64).max:
+                raise GeometryError(f"degenerate element {b // n3} (det <= 0 at node {b % n3})")
+            if source is FactorSource.TRILINEAR_PARTIAL:
+                self._lam_geo = torch.empty((E, n3), dtype=torch.float64, device=dev)
+                _native.check(L.hx_setup_partial(spec.order, E, _ptr(verts), _ptr(self._lam_geo), stream))
+            elif source is FactorSource.TRILINEAR_MERGED:
+                l0, l0v = self._coeff(lam0, E, n3, dev)
+                l1, l1v = self._coeff(lam1, E, n3, dev)
+                self._lam2 = torch.empty((E, n3), dtype=torch.float64, device=dev)
+                self._lam3 = torch.empty((E, n3), dtype=torch.float64, device=dev)
+                _native.check(
+                    L.hx_setup_merged(
+                        spec.order, E, _ptr(verts), _ptr(l0), l0v, _ptr(l1), l1v,
+                        _ptr(self._lam2), _ptr(self._lam3), stream,
+                    )
+                )
+        self._lam0 = self._lam1 = None
+        self._lam0v = self._lam1v = 1.0
+        if helm and source is not FactorSource.TRILINEAR_MERGED:
+            self._lam0, self._lam0v = self._coeff(lam0, E, n3, dev)
+            self._lam1, self._lam1v = self._coeff(lam1, E, n3, dev)
+        self.kernel = 0  # 0 = best available, 1 = generic slice kernel
+
+    # ---- setup helpers -------------------------------------------------
+    @staticmethod
+    def _vertices(elements, dev):
+        """(E,8,3) fp64 device tensor, plus the kind set when known on the host."""
+        torch = _torch()
+        if isinstance(elements, torch.Tensor):
+            if elements.ndim != 3 or tuple(elements.shape[1:]) != (8, 3):
+                raise ValueError("vertex tensor must have shape (E, 8, 3)")
+            return elements.to(device=dev, dtype=torch.float64).contiguous(), None
+        if isinstance(elements, BoxMesh):
+            return elements.vertices_device(dev), None
+        if isinstance(elements, np.ndarray) and elements.ndim == 3:
+            if tuple(elements.shape[1:]) != (8, 3):
+                raise ValueError("vertex array must have shape (E, 8, 3)")
+            return torch.as_tensor(np.ascontiguousarray(elements, dtype=np.float64), device=dev), None
+        elements = list(elements)
+        if not elements:
+            return torch.empty((0, 8, 3), dtype=torch.float64, device=dev), set()
+        kinds = set()
+        for el in elements:
+            kind = getattr(el, "kind", None)
+            kinds.add(_coerce_enum(ElementKind, kind) if kind is not None else ElementKind.GENERAL)
+        host = np.stack([np.asarray(el.vertices, dtype=np.float64) for el in elements])
+        return torch.as_tensor(host, device=dev), kinds
+
+    def _classify(self, verts, stream):
+        torch = _torch()
+        kind = torch.empty((verts.shape[0],), dtype=torch.int8, device=verts.device)
+        _native.check(_native.lib().hx_classify_elements(int(verts.shape[0]), _ptr(verts), _ptr(kind), stream))
+        n_ppd = int(kind.sum().item())
+        out = set()
+        if n_ppd:
+            out.add(ElementKind.PARALLELEPIPED)
+        if n_ppd < verts.shape[0]:
+            out.add(ElementKind.TRILINEAR)
+        return out
+
+    @staticmethod
+    def _coeff(value, E, n3, dev):
+        """(device field or None, scalar) per _coeff_field (axlocal.py:88-101)."""
+        torch = _torch()
+        if value is None:
+            return None, 1.0
+        if isinstance(value, LocalField) or hasattr(value, "data") and hasattr(value, "order"):
+            value = np.asarray(value.data)[:, :, 0]
+        if isinstance(value, torch.Tensor):
+            arr = value.to(device=dev, dtype=torch.float64)
+        else:
+            arr = np.asarray(value, dtype=float)
+            if arr.ndim == 0:
+                return None, float(arr)
+            arr = torch.as_tensor(arr, device=dev)
+        if arr.ndim == 0:
+            return None, float(arr.item())
+        if tuple(arr.shape) == (n3,):
+            return arr.unsqueeze(0).expand(E, n3).contiguous(), 1.0
+        if tuple(arr.shape) != (E, n3):
+            raise ValueError("coefficient field must be scalar or shaped (E, n1**3)")
+        return arr.contiguous(), 1.0
+
+    # ---- apply ---------------------------------------------------------
+    def _args(self, x, y) -> _native.AxArgs:
+        spec = self.spec
+        return _native.AxArgs(
+            order=spec.order,
+            n_col=spec.n_col,
+            equation=0 if spec.equation is Equation.POISSON else 1,
+            factor_source=_HX_SOURCE[spec.factor_source],
+            n_elements=self.n_elements,
+            x=x.data_ptr(),
+            y=y.data_ptr(),
+            verts=self._verts.data_ptr(),
+            h=None if self._h is None else self._h.data_ptr(),
+            g=None if self._g is None else self._g.data_ptr(),
+            gwj=None if self._gwj is None else self._gwj.data_ptr(),
+            lam_geo=None if self._lam_geo is None else self._lam_geo.data_ptr(),
+            lam2=None if self._lam2 is None else self._lam2.data_ptr(),
+            lam3=None if self._lam3 is None else self._lam3.data_ptr(),
+            lam0=None if self._lam0 is None else self._lam0.data_ptr(),
+            lam1=None if self._lam1 is None else self._lam1.data_ptr(),
+            lam0_value=self._lam0v,
+            lam1_value=self._lam1v,
+            kernel=self.kernel,
+            reserved=0,
+        )
+
+    def apply_(self, x, y, stream=None):
+        """y = A x for device tensors (E, n1^3, n_col), stream-ordered, no allocation."""
+        args = self._args(x, y)
+        s = _stream(self.device) if stream is None else ctypes.c_void_p(stream)
+        _native.check(_native.lib().hx_axlocal(ctypes.byref(args), s))
+        return y
+
+    def _check_shape(self, order, n_el, n_col):
+        if order is not None and order != self.spec.order:
+            raise ValueError("field order does not match the operator")
+        if n_el != self.n_elements:
+            raise ValueError("field element count does not match the operator")
+        if n_col != self.spec.n_col:
+            raise ValueError(f"operator expects {self.spec.n_col} column(s)")
+
+    def apply(self, x, threads: int = 1, out=None):
+        """Y = A X.  LocalField in -> LocalField out; CUDA tensor in -> CUDA tensor out."""
+        torch = _torch()
+        n3 = self.basis.n1**3
+        if isinstance(x, torch.Tensor):
+            xt = x if x.ndim == 3 else x.unsqueeze(-1)
+            if xt.ndim != 3 or xt.shape[1] != n3:
+                raise ValueError(f"expected {n3} nodes per element")
+            self._check_shape(None, xt.shape[0], xt.shape[2])
+            xt = xt.to(device=self.device, dtype=torch.float64).contiguous()
+            y = out if out is not None else torch.empty_like(xt)
+            self.apply_(xt, y)
+            return y if x.ndim == 3 else y.squeeze(-1)
+        self._check_shape(x.order, x.n_elements, x.n_col)
+        host = np.ascontiguousarray(x.data, dtype=np.float64)
+        xt = torch.from_numpy(host).pin_memory().to(self.device, non_blocking=True)
+        y = torch.empty_like(xt)
+        self.apply_(xt, y)
+        y_host = torch.empty(y.shape, dtype=torch.float64, pin_memory=True)
+        y_host.copy_(y, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return LocalField(y_host.numpy(), self.spec.order)
+
+
+def ax_local_apply(spec, elements, basis, x, lam0=None, lam1=None, threads: int = 1):
+    """One-shot convenience wrapper around :class:`LocalOperator` (axlocal.py:261-271)."""
+    return LocalOperator(spec, elements, basis, lam0=lam0, lam1=lam1).apply(x, threads)

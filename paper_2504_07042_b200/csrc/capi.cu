@@ -1,0 +1,211 @@
+// extern "C" entry points of libhx_axlocal.so (declared in include/hx_axlocal.h).
+//
+// Validation mirrors the reference's ValueError cases for the apply path
+// (axlocal.py:67-81, 123-127, 238-243); geometry failures are reported through
+// device-side "first bad index" words that the Python layer turns into
+// GeometryError with the reference's messages.
+#include <cstdio>
+#include <string>
+
+#include "hx_common.cuh"
+
+#define HX_VERSION_STRING "hx_axlocal 0.1.0 (sm_100a)"
+
+extern "C" {
+// per-order generic kernels (ax_generic.cu compiled with -DHX_N1=2..16)
+#define HX_DECL_GENERIC(n)                                                                    \
+  cudaError_t hx_generic_launch_##n(const hx_axlocal_args*, cudaStream_t);                   \
+  cudaError_t hx_upload_basis_generic_##n(int, const double*, const double*, const double*);
+HX_DECL_GENERIC(2)
+HX_DECL_GENERIC(3)
+HX_DECL_GENERIC(4)
+HX_DECL_GENERIC(5)
+HX_DECL_GENERIC(6)
+HX_DECL_GENERIC(7)
+HX_DECL_GENERIC(8)
+HX_DECL_GENERIC(9)
+HX_DECL_GENERIC(10)
+HX_DECL_GENERIC(11)
+HX_DECL_GENERIC(12)
+HX_DECL_GENERIC(13)
+HX_DECL_GENERIC(14)
+HX_DECL_GENERIC(15)
+HX_DECL_GENERIC(16)
+cudaError_t hx_upload_basis_setup(int, const double*, const double*, const double*);
+cudaError_t hx_upload_basis_fast(int, const double*, const double*, const double*);
+// specialised kernels (ax_fast.cu): returns cudaErrorNotSupported when no
+// specialised kernel covers the request.
+cudaError_t hx_fast_launch(const hx_axlocal_args*, cudaStream_t);
+
+cudaError_t hx_setup_trilinear_impl(int, int64_t, const double*, int, int64_t*, double*, double*, const double*,
+                                    double, const double*, double, cudaStream_t);
+cudaError_t hx_setup_stored_impl(int, int64_t, const double*, double*, double*, int64_t*, cudaStream_t);
+cudaError_t hx_setup_ppd_impl(int64_t, const double*, double*, int64_t*, cudaStream_t);
+cudaError_t hx_classify_impl(int64_t, const double*, int8_t*, cudaStream_t);
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+
+typedef cudaError_t (*generic_fn)(const hx_axlocal_args*, cudaStream_t);
+typedef cudaError_t (*upload_fn)(int, const double*, const double*, const double*);
+
+const generic_fn kGeneric[hx::kMaxN1 + 1] = {
+    nullptr,
+    nullptr,
+    hx_generic_launch_2,
+    hx_generic_launch_3,
+    hx_generic_launch_4,
+    hx_generic_launch_5,
+    hx_generic_launch_6,
+    hx_generic_launch_7,
+    hx_generic_launch_8,
+    hx_generic_launch_9,
+    hx_generic_launch_10,
+    hx_generic_launch_11,
+    hx_generic_launch_12,
+    hx_generic_launch_13,
+    hx_generic_launch_14,
+    hx_generic_launch_15,
+    hx_generic_launch_16,
+};
+
+const upload_fn kUploads[] = {
+    hx_upload_basis_generic_2,  hx_upload_basis_generic_3,  hx_upload_basis_generic_4,  hx_upload_basis_generic_5,
+    hx_upload_basis_generic_6,  hx_upload_basis_generic_7,  hx_upload_basis_generic_8,  hx_upload_basis_generic_9,
+    hx_upload_basis_generic_10, hx_upload_basis_generic_11, hx_upload_basis_generic_12, hx_upload_basis_generic_13,
+    hx_upload_basis_generic_14, hx_upload_basis_generic_15, hx_upload_basis_generic_16, hx_upload_basis_setup,
+    hx_upload_basis_fast,
+};
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HX_OK;
+  return fail(HX_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool order_ok(int order) { return order >= 1 && order + 1 <= hx::kMaxN1; }
+
+}  // namespace
+
+extern "C" const char* hx_version(void) { return HX_VERSION_STRING; }
+
+extern "C" const char* hx_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int hx_set_basis(int32_t order, const double* points, const double* weights, const double* dmat) {
+  g_last_error.clear();
+  if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (!points || !weights || !dmat) return fail(HX_ERR_INVALID, "hx_set_basis: null basis array");
+  const int n1 = order + 1;
+  for (upload_fn f : kUploads) {
+    int st = cuda_status(f(n1, points, weights, dmat), "hx_set_basis");
+    if (st) return st;
+  }
+  return cuda_status(cudaDeviceSynchronize(), "hx_set_basis");
+}
+
+extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
+  g_last_error.clear();
+  if (!a) return fail(HX_ERR_INVALID, "null args");
+  if (!order_ok(a->order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (a->n_col != 1 && a->n_col != 3) return fail(HX_ERR_INVALID, "n_col must be 1 or 3");
+  if (a->equation != HX_POISSON && a->equation != HX_HELMHOLTZ) return fail(HX_ERR_INVALID, "bad equation");
+  if (a->factor_source < HX_STORED || a->factor_source > HX_PARALLELEPIPED)
+    return fail(HX_ERR_INVALID, "bad factor source");
+  const bool helm = a->equation == HX_HELMHOLTZ;
+  if (a->factor_source == HX_TRILINEAR_MERGED && !helm)
+    return fail(HX_ERR_INVALID, "the merged-scalar variant exists for Helmholtz only");
+  if (a->factor_source == HX_TRILINEAR_PARTIAL && helm)
+    return fail(HX_ERR_INVALID, "the partial-recompute variant exists for Poisson only");
+  if (a->n_elements < 0) return fail(HX_ERR_INVALID, "negative element count");
+  if (a->n_elements == 0) return HX_OK;
+  if (!a->x || !a->y) return fail(HX_ERR_INVALID, "null x or y");
+  switch (a->factor_source) {
+    case HX_STORED:
+      if (!a->g || (helm && !a->gwj)) return fail(HX_ERR_INVALID, "stored factors missing");
+      break;
+    case HX_PARALLELEPIPED:
+      if (!a->h) return fail(HX_ERR_INVALID, "parallelepiped constants missing");
+      break;
+    case HX_TRILINEAR:
+      if (!a->verts) return fail(HX_ERR_INVALID, "vertices missing");
+      break;
+    case HX_TRILINEAR_MERGED:
+      if (!a->verts || !a->lam2 || !a->lam3) return fail(HX_ERR_INVALID, "merged scalars missing");
+      break;
+    case HX_TRILINEAR_PARTIAL:
+      if (!a->verts || !a->lam_geo) return fail(HX_ERR_INVALID, "partial lam_geo missing");
+      break;
+  }
+  if (!helm && (a->lam0 || a->lam1))
+    return fail(HX_ERR_INVALID, "coefficient fields apply to the Helmholtz operator only");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n1 = a->order + 1;
+  if (a->kernel != 1) {
+    cudaError_t e = hx_fast_launch(a, s);
+    if (e != cudaErrorNotSupported) return cuda_status(e, "hx_axlocal(fast)");
+    (void)cudaGetLastError();
+  }
+  if (n1 < 2) {
+    // order must be >= 1 so n1 >= 2 always; kept for clarity
+    return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  }
+  return cuda_status(kGeneric[n1](a, s), "hx_axlocal(generic)");
+}
+
+extern "C" int hx_trilinear_validate(int32_t order, int64_t E, const double* verts, int64_t* first_bad,
+                                     void* stream) {
+  g_last_error.clear();
+  if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (!verts || !first_bad) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_setup_trilinear_impl(order + 1, E, verts, 0, first_bad, nullptr, nullptr, nullptr, 1.0,
+                                             nullptr, 1.0, static_cast<cudaStream_t>(stream)),
+                     "hx_trilinear_validate");
+}
+
+extern "C" int hx_setup_partial(int32_t order, int64_t E, const double* verts, double* lam_geo, void* stream) {
+  g_last_error.clear();
+  if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (!verts || !lam_geo) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_setup_trilinear_impl(order + 1, E, verts, 1, nullptr, lam_geo, nullptr, nullptr, 1.0,
+                                             nullptr, 1.0, static_cast<cudaStream_t>(stream)),
+                     "hx_setup_partial");
+}
+
+extern "C" int hx_setup_merged(int32_t order, int64_t E, const double* verts, const double* lam0, double l0v,
+                               const double* lam1, double l1v, double* lam2, double* lam3, void* stream) {
+  g_last_error.clear();
+  if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (!verts || !lam2 || !lam3) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_setup_trilinear_impl(order + 1, E, verts, 2, nullptr, lam2, lam3, lam0, l0v, lam1, l1v,
+                                             static_cast<cudaStream_t>(stream)),
+                     "hx_setup_merged");
+}
+
+extern "C" int hx_setup_stored(int32_t order, int64_t E, const double* verts, double* g, double* gwj,
+                               int64_t* first_bad, void* stream) {
+  g_last_error.clear();
+  if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (!verts || !g || !first_bad) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(
+      hx_setup_stored_impl(order + 1, E, verts, g, gwj, first_bad, static_cast<cudaStream_t>(stream)),
+      "hx_setup_stored");
+}
+
+extern "C" int hx_setup_parallelepiped(int64_t E, const double* verts, double* h, int64_t* bad, void* stream) {
+  g_last_error.clear();
+  if (!verts || !h || !bad) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_setup_ppd_impl(E, verts, h, bad, static_cast<cudaStream_t>(stream)),
+                     "hx_setup_parallelepiped");
+}
+
+extern "C" int hx_classify_elements(int64_t E, const double* verts, int8_t* kind, void* stream) {
+  g_last_error.clear();
+  if (!verts || !kind) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_classify_impl(E, verts, kind, static_cast<cudaStream_t>(stream)), "hx_classify_elements");
+}
