@@ -281,36 +281,46 @@ class LocalOperator:
         return arr.contiguous(), 1.0
 
     # ---- apply ---------------------------------------------------------
-    def _args(self, x, y) -> _native.AxArgs:
+    def _args(self, x_ptr, y_ptr, e0=0, n=None) -> _native.AxArgs:
+        """Kernel arguments for elements [e0, e0+n); x_ptr/y_ptr point at element e0."""
         spec = self.spec
+        n = self.n_elements - e0 if n is None else n
+        n3 = self.basis.n1**3
+
+        def off(t, per):
+            return None if t is None else t.data_ptr() + 8 * per * e0
+
         return _native.AxArgs(
             order=spec.order,
             n_col=spec.n_col,
             equation=0 if spec.equation is Equation.POISSON else 1,
             factor_source=_HX_SOURCE[spec.factor_source],
-            n_elements=self.n_elements,
-            x=x.data_ptr(),
-            y=y.data_ptr(),
-            verts=self._verts.data_ptr(),
-            h=None if self._h is None else self._h.data_ptr(),
-            g=None if self._g is None else self._g.data_ptr(),
-            gwj=None if self._gwj is None else self._gwj.data_ptr(),
-            lam_geo=None if self._lam_geo is None else self._lam_geo.data_ptr(),
-            lam2=None if self._lam2 is None else self._lam2.data_ptr(),
-            lam3=None if self._lam3 is None else self._lam3.data_ptr(),
-            lam0=None if self._lam0 is None else self._lam0.data_ptr(),
-            lam1=None if self._lam1 is None else self._lam1.data_ptr(),
+            n_elements=n,
+            x=x_ptr,
+            y=y_ptr,
+            verts=off(self._verts, 24),
+            h=off(self._h, 7),
+            g=off(self._g, 6 * n3),
+            gwj=off(self._gwj, n3),
+            lam_geo=off(self._lam_geo, n3),
+            lam2=off(self._lam2, n3),
+            lam3=off(self._lam3, n3),
+            lam0=off(self._lam0, n3),
+            lam1=off(self._lam1, n3),
             lam0_value=self._lam0v,
             lam1_value=self._lam1v,
             kernel=self.kernel,
             reserved=0,
         )
 
-    def apply_(self, x, y, stream=None):
-        """y = A x for device tensors (E, n1^3, n_col), stream-ordered, no allocation."""
-        args = self._args(x, y)
+    def _launch(self, args, stream=None):
         s = _stream(self.device) if stream is None else ctypes.c_void_p(stream)
         _native.check(_native.lib().hx_axlocal(ctypes.byref(args), s))
+
+    def apply_(self, x, y, stream=None):
+        """y = A x for contiguous fp64 device tensors (E, n1^3, n_col); stream-ordered,
+        no allocation, no synchronisation."""
+        self._launch(self._args(x.data_ptr(), y.data_ptr()), stream)
         return y
 
     def _check_shape(self, order, n_el, n_col):
@@ -322,7 +332,14 @@ class LocalOperator:
             raise ValueError(f"operator expects {self.spec.n_col} column(s)")
 
     def apply(self, x, threads: int = 1, out=None):
-        """Y = A X.  LocalField in -> LocalField out; CUDA tensor in -> CUDA tensor out."""
+        """Y = A X.
+
+        * ``LocalField`` (host numpy, the reference's type) -> ``LocalField``;
+        * CUDA tensor (E, n1^3, n_col) or (E, n1^3) -> CUDA tensor (no copies);
+        * host torch tensor (pinned for full speed) -> host tensor, through a
+          chunked pipeline that overlaps the H2D copy of chunk c+1, the kernel on
+          chunk c and the D2H copy of chunk c-1.
+        """
         torch = _torch()
         n3 = self.basis.n1**3
         if isinstance(x, torch.Tensor):
@@ -330,19 +347,48 @@ class LocalOperator:
             if xt.ndim != 3 or xt.shape[1] != n3:
                 raise ValueError(f"expected {n3} nodes per element")
             self._check_shape(None, xt.shape[0], xt.shape[2])
+            if not xt.is_cuda:
+                y = self._apply_host(xt.to(torch.float64).contiguous(), out)
+                return y if x.ndim == 3 else y.squeeze(-1)
             xt = xt.to(device=self.device, dtype=torch.float64).contiguous()
             y = out if out is not None else torch.empty_like(xt)
             self.apply_(xt, y)
             return y if x.ndim == 3 else y.squeeze(-1)
         self._check_shape(x.order, x.n_elements, x.n_col)
-        host = np.ascontiguousarray(x.data, dtype=np.float64)
-        xt = torch.from_numpy(host).pin_memory().to(self.device, non_blocking=True)
-        y = torch.empty_like(xt)
-        self.apply_(xt, y)
-        y_host = torch.empty(y.shape, dtype=torch.float64, pin_memory=True)
-        y_host.copy_(y, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        return LocalField(y_host.numpy(), self.spec.order)
+        host = torch.from_numpy(np.ascontiguousarray(x.data, dtype=np.float64))
+        y = self._apply_host(host, None)
+        return LocalField(y.numpy(), self.spec.order)
+
+    def _apply_host(self, xh, out):
+        torch = _torch()
+        dev = self.device
+        if not xh.is_pinned():
+            xh = xh.pin_memory()
+        yh = out if out is not None else torch.empty(xh.shape, dtype=torch.float64, pin_memory=True)
+        bufs = getattr(self, "_dev_bufs", None)
+        if bufs is None or bufs[0].shape != xh.shape:
+            bufs = (torch.empty(xh.shape, dtype=torch.float64, device=dev),
+                    torch.empty(xh.shape, dtype=torch.float64, device=dev),
+                    torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+            self._dev_bufs = bufs
+        xd, yd, s_in, s_out = bufs
+        cur = torch.cuda.current_stream(dev)
+        E = self.n_elements
+        chunk = max(1024, -(-E // 16))
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        for a in range(0, E, chunk):
+            b = min(E, a + chunk)
+            with torch.cuda.stream(s_in):
+                xd[a:b].copy_(xh[a:b], non_blocking=True)
+            cur.wait_stream(s_in)
+            self._launch(self._args(xd[a].data_ptr(), yd[a].data_ptr(), a, b - a), cur.cuda_stream)
+            s_out.wait_stream(cur)
+            with torch.cuda.stream(s_out):
+                yh[a:b].copy_(yd[a:b], non_blocking=True)
+        cur.wait_stream(s_out)
+        s_out.synchronize()
+        return yh
 
 
 def ax_local_apply(spec, elements, basis, x, lam0=None, lam1=None, threads: int = 1):

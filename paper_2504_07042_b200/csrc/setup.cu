@@ -64,62 +64,72 @@ __device__ __forceinline__ double node_coord(const double v[24], const double* x
 
 // Stored (general-route) factors: collocation Jacobian + dense inverse
 // (discrete_jacobians + factors_from_jacobians, geometry.py:225-276).
+// One block per element: node coordinates staged in shared memory, then each
+// thread contracts them with D for its nodes.
 __global__ void stored_setup_kernel(int n1, int64_t E, const double* __restrict__ verts, double* g_out,
                                     double* gwj_out, int64_t* first_bad) {
+  extern __shared__ double s_xyz[];  // [3][n3]
   const int n3 = n1 * n1 * n1;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= E * n3) return;
-  const int64_t e = gid / n3;
-  const int node = (int)(gid % n3);
-  const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+  const int64_t e = blockIdx.x;
   const int od = off_d(n1), op = off_p(n1);
   const double* xi = c_X + op;
   double v[24];
   for (int q = 0; q < 24; ++q) v[q] = verts[e * 24 + q];
-  double jac[3][3];  // jac[a][b] = d x_a / d r_b
-  for (int c = 0; c < 3; ++c) {
-    double dr = 0.0, ds = 0.0, dt = 0.0;
-    for (int n = 0; n < n1; ++n) {
-      dr += c_D[od + i * n1 + n] * node_coord(v, xi, n, j, k, c);
-      ds += c_D[od + j * n1 + n] * node_coord(v, xi, i, n, k, c);
-      dt += c_D[od + k * n1 + n] * node_coord(v, xi, i, j, n, c);
+  for (int node = threadIdx.x; node < n3; node += blockDim.x) {
+    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+    for (int c = 0; c < 3; ++c) s_xyz[c * n3 + node] = node_coord(v, xi, i, j, k, c);
+  }
+  __syncthreads();
+  for (int node = threadIdx.x; node < n3; node += blockDim.x) {
+    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+    double jac[3][3];  // jac[a][b] = d x_a / d r_b
+    for (int c = 0; c < 3; ++c) {
+      const double* X = s_xyz + c * n3;
+      double dr = 0.0, ds = 0.0, dt = 0.0;
+      for (int n = 0; n < n1; ++n) {
+        dr += c_D[od + i * n1 + n] * X[(k * n1 + j) * n1 + n];
+        ds += c_D[od + j * n1 + n] * X[(k * n1 + n) * n1 + i];
+        dt += c_D[od + k * n1 + n] * X[(n * n1 + j) * n1 + i];
+      }
+      jac[c][0] = dr;
+      jac[c][1] = ds;
+      jac[c][2] = dt;
     }
-    jac[c][0] = dr;
-    jac[c][1] = ds;
-    jac[c][2] = dt;
+    const double c0[3] = {jac[0][0], jac[1][0], jac[2][0]};
+    const double c1[3] = {jac[0][1], jac[1][1], jac[2][1]};
+    const double c2[3] = {jac[0][2], jac[1][2], jac[2][2]};
+    const double det = det3_cols(c0, c1, c2);
+    const int64_t gid = e * n3 + node;
+    if (det <= 0.0 || det != det) {
+      atomic_min_i64(first_bad, gid);
+      continue;
+    }
+    // inverse = adj(jac) / det
+    double inv[3][3];
+    inv[0][0] = (jac[1][1] * jac[2][2] - jac[1][2] * jac[2][1]) / det;
+    inv[0][1] = (jac[0][2] * jac[2][1] - jac[0][1] * jac[2][2]) / det;
+    inv[0][2] = (jac[0][1] * jac[1][2] - jac[0][2] * jac[1][1]) / det;
+    inv[1][0] = (jac[1][2] * jac[2][0] - jac[1][0] * jac[2][2]) / det;
+    inv[1][1] = (jac[0][0] * jac[2][2] - jac[0][2] * jac[2][0]) / det;
+    inv[1][2] = (jac[0][2] * jac[1][0] - jac[0][0] * jac[1][2]) / det;
+    inv[2][0] = (jac[1][0] * jac[2][1] - jac[1][1] * jac[2][0]) / det;
+    inv[2][1] = (jac[0][1] * jac[2][0] - jac[0][0] * jac[2][1]) / det;
+    inv[2][2] = (jac[0][0] * jac[1][1] - jac[0][1] * jac[1][0]) / det;
+    double m[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int c = 0; c < 3; ++c)
+        m[a][c] = inv[a][0] * inv[c][0] + inv[a][1] * inv[c][1] + inv[a][2] * inv[c][2];
+    const double w = c_W[op + k] * c_W[op + j] * c_W[op + i];
+    const double scale = w * det;
+    double* g = g_out + e * 6 * n3 + node;
+    g[0 * n3] = scale * m[0][0];
+    g[1 * n3] = scale * m[0][1];
+    g[2 * n3] = scale * m[0][2];
+    g[3 * n3] = scale * m[1][1];
+    g[4 * n3] = scale * m[1][2];
+    g[5 * n3] = scale * m[2][2];
+    if (gwj_out) gwj_out[gid] = scale;
   }
-  const double c0[3] = {jac[0][0], jac[1][0], jac[2][0]};
-  const double c1[3] = {jac[0][1], jac[1][1], jac[2][1]};
-  const double c2[3] = {jac[0][2], jac[1][2], jac[2][2]};
-  const double det = det3_cols(c0, c1, c2);
-  if (det <= 0.0 || det != det) {
-    atomic_min_i64(first_bad, gid);
-    return;
-  }
-  // inverse = adj(jac) / det
-  double inv[3][3];
-  inv[0][0] = (jac[1][1] * jac[2][2] - jac[1][2] * jac[2][1]) / det;
-  inv[0][1] = (jac[0][2] * jac[2][1] - jac[0][1] * jac[2][2]) / det;
-  inv[0][2] = (jac[0][1] * jac[1][2] - jac[0][2] * jac[1][1]) / det;
-  inv[1][0] = (jac[1][2] * jac[2][0] - jac[1][0] * jac[2][2]) / det;
-  inv[1][1] = (jac[0][0] * jac[2][2] - jac[0][2] * jac[2][0]) / det;
-  inv[1][2] = (jac[0][2] * jac[1][0] - jac[0][0] * jac[1][2]) / det;
-  inv[2][0] = (jac[1][0] * jac[2][1] - jac[1][1] * jac[2][0]) / det;
-  inv[2][1] = (jac[0][1] * jac[2][0] - jac[0][0] * jac[2][1]) / det;
-  inv[2][2] = (jac[0][0] * jac[1][1] - jac[0][1] * jac[1][0]) / det;
-  double m[3][3];
-  for (int a = 0; a < 3; ++a)
-    for (int c = 0; c < 3; ++c) m[a][c] = inv[a][0] * inv[c][0] + inv[a][1] * inv[c][1] + inv[a][2] * inv[c][2];
-  const double w = c_W[op + k] * c_W[op + j] * c_W[op + i];
-  const double scale = w * det;
-  double* g = g_out + e * 6 * n3 + node;
-  g[0 * n3] = scale * m[0][0];
-  g[1 * n3] = scale * m[0][1];
-  g[2 * n3] = scale * m[0][2];
-  g[3 * n3] = scale * m[1][1];
-  g[4 * n3] = scale * m[1][2];
-  g[5 * n3] = scale * m[2][2];
-  if (gwj_out) gwj_out[gid] = scale;
 }
 
 __device__ __forceinline__ double ppd_defect(const double* v, double& scale) {
@@ -216,8 +226,15 @@ extern "C" cudaError_t hx_setup_trilinear_impl(int n1, int64_t E, const double* 
 extern "C" cudaError_t hx_setup_stored_impl(int n1, int64_t E, const double* verts, double* g, double* gwj,
                                             int64_t* first_bad, cudaStream_t s) {
   hx::init_i64<<<1, 1, 0, s>>>(first_bad, INT64_MAX);
-  const int64_t n = E * n1 * n1 * n1;
-  if (n > 0) hx::stored_setup_kernel<<<hx::grid_for(n, 128), 128, 0, s>>>(n1, E, verts, g, gwj, first_bad);
+  const int n3 = n1 * n1 * n1;
+  const size_t smem = sizeof(double) * 3 * n3;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(hx::stored_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  // grid.x <= 2^31-1 elements
+  if (E > 0) hx::stored_setup_kernel<<<(unsigned)E, n3 < 256 ? n3 : 256, smem, s>>>(n1, E, verts, g, gwj, first_bad);
   return cudaGetLastError();
 }
 
