@@ -1,0 +1,87 @@
+"""Kernel-variant timing sweep on one GPU (development tool, not the bench).
+
+    python tools/sweep.py [--mesh 128,128,96] [--reps 20]
+
+Times every (variant, kernel path, tuning hook) at N=7 with CUDA events on a
+resident x/y and prints GDOF/s, TFLOP/s (algorithmic) and HBM GB/s.
+"""
+
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2504_07042_b200 as hx  # noqa: E402
+from paper_2504_07042_b200.workload import workload_count  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mesh", default="128,128,96")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--order", type=int, default=7)
+    ap.add_argument("--only", default=None)
+    args = ap.parse_args()
+    ex, ey, ez = (int(v) for v in args.mesh.split(","))
+    order = args.order
+    dev = torch.device("cuda", 0)
+    mesh = hx.box_mesh(ex, ey, ez, order, perturbation=0.1, seed=0)
+    verts = mesh.vertices_device(dev)
+    shear = torch.tensor([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]], dtype=torch.float64, device=dev)
+    verts_ppd = hx.box_mesh(ex, ey, ez, order).vertices_device(dev) @ shear.T
+    E = verts.shape[0]
+    n3 = (order + 1) ** 3
+    basis = hx.SpectralBasis.build(order)
+    rows = []
+    cases = [
+        ("poisson", 1, "trilinear", 0, 0),
+        ("poisson", 1, "trilinear", 0, 4),
+        ("poisson", 1, "trilinear", 0, 5),
+        ("poisson", 1, "trilinear", 0, 8),
+        ("poisson", 1, "trilinear", 1, 0),
+        ("poisson", 1, "trilinear-partial", 0, 0),
+        ("poisson", 1, "stored", 0, 0),
+        ("poisson", 1, "stored", 1, 0),
+        ("poisson", 1, "parallelepiped", 0, 0),
+        ("helmholtz", 1, "trilinear", 0, 0),
+        ("helmholtz", 1, "trilinear-merged", 0, 0),
+        ("poisson", 3, "trilinear", 0, 0),
+    ]
+    for eq, ncol, src, kernel, hook in cases:
+        if args.only and args.only not in src:
+            continue
+        spec = hx.KernelSpec(eq, ncol, src, order)
+        v = verts_ppd if src == "parallelepiped" else verts
+        ee = E if ncol == 1 else E // 3
+        op = hx.LocalOperator(spec, v[:ee], basis, device=dev)
+        op.kernel = kernel
+        x = torch.randn((ee, n3, ncol), dtype=torch.float64, device=dev)
+        y = torch.empty_like(x)
+        args_c = op._args(x.data_ptr(), y.data_ptr())
+        args_c.reserved = hook
+        for _ in range(3):
+            op._launch(args_c)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.reps):
+            op._launch(args_c)
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e) / args.reps
+        wc = workload_count(spec, include_dmat_traffic=False)
+        gdofs = ee * n3 * ncol / (ms * 1e-3) / 1e9
+        tf = ee * (wc.f_ax + wc.f_geo) / (ms * 1e-3) / 1e12
+        gbs = ee * wc.m_bytes / (ms * 1e-3) / 1e9
+        row = f"{eq:9s} ncol={ncol} {src:18s} kernel={'fast' if kernel == 0 else 'generic'} hook={hook}: " \
+              f"{ms:8.3f} ms  {gdofs:7.1f} GDOF/s  {tf:6.2f} TFLOP/s  {gbs:7.1f} GB/s"
+        print(row, flush=True)
+        rows.append(row)
+        del op, x, y
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
