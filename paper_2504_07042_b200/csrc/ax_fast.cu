@@ -1,23 +1,27 @@
 // Specialised AxLocal kernel for N = 7 (n1 = 8), the north-star order.
 //
-// One 64-thread CTA per element.  The FP64 pipe (DFMA and DMMA share it on
-// B200, tools/ubench_fp64.cu) is the bound, so the design minimises FP64
-// operations and keeps shared memory under the pipe time:
+// Persistent 64-thread CTAs, one element at a time, the next element's x (and
+// vertices) prefetched by a 1-D bulk async copy (TMA, cp.async.bulk) into a
+// double-buffered landing zone tracked by mbarriers.  The FP64 pipe (DFMA and
+// DMMA share it on B200, tools/ubench_fp64.cu) is the bound, so the design
+// minimises FP64 operations and keeps shared memory below the pipe time:
 //
 //  * contractions by even-odd decomposition: D and D^T are centro-
-//    antisymmetric on GLL points, so an 8-point contraction is 8 adds +
-//    two 4x4 products + 8 adds = 48 ops instead of 64 (the 4x4 blocks sit in
-//    __constant__ and are DFMA operands at compile-time offsets);
-//  * three pencil ownerships per element (k-fibres, i-rows, j-columns); the
-//    element cube moves between them through shared memory with the additive
-//    layout a(k,j,i) = Ak[k] + Aj[j] + i, conflict-free for all three access
-//    patterns (DESIGN.md derives it);
+//    antisymmetric on GLL points, so an 8-point contraction is 8 adds + two
+//    4x4 products + 8 adds = 48 ops instead of 64, the 4x4 blocks read as
+//    __constant__ operands at compile-time offsets;
+//  * three fibre ownerships per element (k-fibres, i-rows, j-columns); the
+//    cube moves between them through shared memory laid out as
+//    a(k,j,i) = Ak[k] + Aj[j] + i with lane->fibre maps chosen so every
+//    64-bit access of every phase hits 16 distinct bank pairs per half-warp
+//    (no conflicts; DESIGN.md derives it) — including the k-fibre read of the
+//    linear TMA landing buffer;
 //  * trilinear geometry (Algorithm 2) as polynomials in the
-//    reference coordinate t along each k-fibre: K00, K01, K11 are quadratic,
-//    K02, K12 linear, K22 constant, det(JT) quadratic, so a node costs 8 FMAs
-//    for K, 12 for adj(K), 2 for det and one reciprocal (MUFU + 3 FMAs)
-//    instead of re-evaluating the Jacobian columns;
-//  * D, tensor weights and points never touch shared memory.
+//    reference coordinate t along each k-fibre: K00, K01, K11 quadratic, K02,
+//    K12 linear, K22 constant and det(JT) quadratic, so a node costs 8 FMAs
+//    for K, 12 for adj(K), 2 for det and a MUFU reciprocal with one cubic
+//    correction; the per-element pieces that depend on j only or i only are
+//    computed once per element and shared through shared memory.
 //
 // The arithmetic differs from the reference's operation order, so parity is
 // to the 1e-12 relative bar, not bitwise; per-column arithmetic is identical
@@ -29,11 +33,29 @@ namespace fast {
 
 constexpr int N1 = 8;
 constexpr int N3 = 512;
-constexpr int CUBE = 576;  // 575 used, rounded up
-
+constexpr int CUBE = 544;  // 543 used
 
 __host__ __device__ constexpr int Aj(int j) { return 17 * (j >> 1) + 8 * (j & 1); }
-__host__ __device__ constexpr int Ak(int k) { return 144 * (k >> 1) + 72 * (k & 1) + 4 * ((k >> 1) & 1); }
+__host__ __device__ constexpr int Ak(int k) { return 68 * k; }
+
+// lane -> fibre maps
+struct Roles {
+  int fi, fj;  // k-fibre (i, j)
+  int rj, rk;  // i-row (j, k)
+  int ci, ck;  // j-column (i, k)
+};
+
+__device__ __forceinline__ Roles roles(int t) {
+  const int w = t >> 5, l = t & 31, h = l >> 4, p = (l >> 3) & 1, q = l & 15;
+  Roles r;
+  r.fi = l & 7;
+  r.fj = 4 * w + 2 * h + p;
+  r.rj = 2 * (q & 3) + h;
+  r.rk = 4 * w + (q >> 2);
+  r.ci = l & 7;
+  r.ck = 4 * w + h + 2 * p;
+  return r;
+}
 
 }  // namespace fast
 }  // namespace hx
@@ -68,64 +90,125 @@ __device__ __forceinline__ void eo8(const double v[8], double out[8]) {
   }
 }
 
-// 1/d from the MUFU seed and one cubic correction: r (1 + e + e^2), e = 1 - d r.
-__device__ __forceinline__ double rcp_fast(double d) {
+// w / d: MUFU reciprocal seed r, e = 1 - d r, w r (1 + e + e^2)  (error ~ e^3).
+__device__ __forceinline__ double div_fast(double w, double d) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
   const double e = fma(-d, r, 1.0);
-  return fma(fma(e, e, e), r, r);
+  const double wr = w * r;
+  return fma(fma(e, e, e), wr, wr);
 }
 
-struct Fibre {
-  int i, j;  // k-fibre owner
+// Per-element trilinear pieces shared by the 64 fibres (written by 28 threads).
+struct TriShared {
+  double j[8][6];  // dr_base[3], dr_slope[3] per j
+  double i[8][6];  // ds_base[3], ds_slope[3] per i
+  double d[12];     // v4-v0, v5-v1, v7-v3, v6-v2
 };
 
-// ---------------------------------------------------------------------------
-// factor policies: prepare() once per element (after vertices are in smem),
-// node(k, x0, x1, x2, &rr, &ss, &tt, &mass_scale) per node of the k-fibre.
+__device__ __forceinline__ double dot3(const double* u, const double* v) {
+  return u[0] * v[0] + u[1] * v[1] + u[2] * v[2];
+}
 
-// Trilinear recompute (geometry.py:304-351; axlocal.py:191-201), polynomial in t.
-template <bool HELM, bool MERGED, bool PARTIAL>
+// Stage A: common_terms (geometry.py:135-184) split into 60 short independent
+// tasks (one coordinate of one j-side or i-side base/slope pair, or one vertex
+// difference), so no thread runs a long dependent chain while the others wait.
+__device__ __forceinline__ void tri_stage_a(int t, const double* __restrict__ v, TriShared& s) {
+  if (t < 48) {
+    const bool jside = t < 24;
+    const int task = jside ? t : t - 24;
+    const int idx = task / 3, c = task % 3;
+    const double xi = cX<N1>(idx);
+    const double a0 = 1.0 - xi, a1 = 1.0 + xi;
+    // j side: tmp1 = a0 (v1-v0) + a1 (v3-v2), tmp2 = a0 (v5-v4) + a1 (v7-v6)
+    // i side: tmp3 = a0 (v2-v0) + a1 (v3-v1), tmp4 = a0 (v6-v4) + a1 (v7-v5)
+    const int p0 = jside ? 1 : 2, p1 = 3, q1 = jside ? 2 : 1;
+    const int p2 = jside ? 5 : 6, p3 = 7, q3 = jside ? 6 : 5;
+    const double lo = a0 * (v[p0 * 3 + c] - v[c]) + a1 * (v[p1 * 3 + c] - v[q1 * 3 + c]);
+    const double hi = a0 * (v[p2 * 3 + c] - v[12 + c]) + a1 * (v[p3 * 3 + c] - v[q3 * 3 + c]);
+    double* out = jside ? s.j[idx] : s.i[idx];
+    out[c] = lo + hi;
+    out[3 + c] = hi - lo;
+  } else if (t < 60) {
+    const int q = t - 48, pair = q / 3, c = q % 3;
+    const int pa = pair == 0 ? 4 : pair == 1 ? 5 : pair == 2 ? 7 : 6;
+    const int pb = pair == 0 ? 0 : pair == 1 ? 1 : pair == 2 ? 3 : 2;
+    s.d[q] = v[pa * 3 + c] - v[pb * 3 + c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// factor policies: prepare() once per element (after TriShared is written),
+// node<K>(...) per node of the k-fibre.
+
+// Trilinear recompute (geometry.py:304-351; axlocal.py:191-211), polynomial in t.
+template <bool HELM, bool MERGED, bool PARTIAL, bool SHARED = true>
 struct TrilinearPoly {
+  static constexpr bool kStageA = SHARED;
   double k00[3], k11[3], k01[3], k02[2], k12[2], k22, det[3];
-  double w_ji;  // w_j * w_i with the k weight applied per node: (w_k w_j) w_i
-  double wj, wi;
+  double wji8;
   const double* lam_a;  // partial: lam_geo; merged: lam2; trilinear-helm: lam0 (or null)
   const double* lam_b;  // merged: lam3; trilinear-helm: lam1 (or null)
   double l0v, l1v;
 
-  __device__ void prepare(const hx_axlocal_args& a, int64_t e, const double* sv, Fibre f) {
-    const double xi = cX<N1>(f.i), xj = cX<N1>(f.j);
-    TrilinearPencil p;
-    trilinear_pencil(sv, xi, xj, p);
-    const double* br = p.dr_base;
-    const double* sr = p.dr_slope;
-    const double* bs = p.ds_base;
-    const double* ss = p.ds_slope;
-    const double* c = p.dt_col;
-    auto dot = [](const double* u, const double* v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; };
-    k00[0] = dot(br, br);
-    k00[1] = 2.0 * dot(br, sr);
-    k00[2] = dot(sr, sr);
-    k11[0] = dot(bs, bs);
-    k11[1] = 2.0 * dot(bs, ss);
-    k11[2] = dot(ss, ss);
-    k01[0] = dot(br, bs);
-    k01[1] = dot(br, ss) + dot(sr, bs);
-    k01[2] = dot(sr, ss);
-    k02[0] = dot(br, c);
-    k02[1] = dot(sr, c);
-    k12[0] = dot(bs, c);
-    k12[1] = dot(ss, c);
-    k22 = dot(c, c);
-    // det = (br + t sr) . ((bs + t ss) x c)
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, int64_t e, const TriShared& s,
+                                          const double* sv, int fi, int fj) {
+    double br[3], sr[3], bs[3], ss[3], c[3];
+    if (SHARED) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        br[q] = s.j[fj][q];
+        sr[q] = s.j[fj][3 + q];
+        bs[q] = s.i[fi][q];
+        ss[q] = s.i[fi][3 + q];
+      }
+    } else {
+      TrilinearPencil p;
+      trilinear_pencil(sv, cX<N1>(fi), cX<N1>(fj), p);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        br[q] = p.dr_base[q];
+        sr[q] = p.dr_slope[q];
+        bs[q] = p.ds_base[q];
+        ss[q] = p.ds_slope[q];
+      }
+    }
+    k00[0] = dot3(br, br);
+    k00[1] = 2.0 * dot3(br, sr);
+    k00[2] = dot3(sr, sr);
+    k11[0] = dot3(bs, bs);
+    k11[1] = 2.0 * dot3(bs, ss);
+    k11[2] = dot3(ss, ss);
+    if (SHARED) {
+      const double xj = cX<N1>(fj), xi = cX<N1>(fi);
+      const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
+      const double w00 = a0j * a0i, w01 = a0j * a1i, w10 = a1j * a0i, w11 = a1j * a1i;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) c[q] = w00 * s.d[q] + w01 * s.d[3 + q] + w11 * s.d[6 + q] + w10 * s.d[9 + q];
+    } else {
+      const double xj = cX<N1>(fj), xi = cX<N1>(fi);
+      const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
+      const double w00 = a0j * a0i, w01 = a0j * a1i, w10 = a1j * a0i, w11 = a1j * a1i;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        c[q] = w00 * (sv[12 + q] - sv[q]) + w01 * (sv[15 + q] - sv[3 + q]) + w11 * (sv[21 + q] - sv[9 + q]) +
+               w10 * (sv[18 + q] - sv[6 + q]);
+    }
+    k01[0] = dot3(br, bs);
+    k01[1] = dot3(br, ss) + dot3(sr, bs);
+    k01[2] = dot3(sr, ss);
+    k02[0] = dot3(br, c);
+    k02[1] = dot3(sr, c);
+    k12[0] = dot3(bs, c);
+    k12[1] = dot3(ss, c);
+    k22 = dot3(c, c);
+    // det(JT) = (br + t sr) . ((bs + t ss) x c)
     const double P[3] = {bs[1] * c[2] - bs[2] * c[1], bs[2] * c[0] - bs[0] * c[2], bs[0] * c[1] - bs[1] * c[0]};
     const double Q[3] = {ss[1] * c[2] - ss[2] * c[1], ss[2] * c[0] - ss[0] * c[2], ss[0] * c[1] - ss[1] * c[0]};
-    det[0] = dot(br, P);
-    det[1] = dot(br, Q) + dot(sr, P);
-    det[2] = dot(sr, Q);
-    wj = cW<N1>(f.j);
-    wi = cW<N1>(f.i);
+    det[0] = dot3(br, P);
+    det[1] = dot3(br, Q) + dot3(sr, P);
+    det[2] = dot3(sr, Q);
+    wji8 = 0.125 * (cW<N1>(fj) * cW<N1>(fi));
     lam_a = lam_b = nullptr;
     l0v = a.lam0_value;
     l1v = a.lam1_value;
@@ -141,8 +224,8 @@ struct TrilinearPoly {
   }
 
   template <int K>
-  __device__ __forceinline__ void node(int nodeidx, double x0, double x1, double x2, double& rr, double& ss,
-                                       double& tt, double& mass) const {
+  __device__ __forceinline__ void node(int n, double x0, double x1, double x2, double& rr, double& ss, double& tt,
+                                       double& mass) const {
     const double t = cX<N1>(K);
     const double a00 = fma(fma(k00[2], t, k00[1]), t, k00[0]);
     const double a11 = fma(fma(k11[2], t, k11[1]), t, k11[0]);
@@ -158,16 +241,16 @@ struct TrilinearPoly {
     double scale;
     mass = 0.0;
     if (MERGED) {
-      scale = __ldg(lam_a + nodeidx);
-      mass = __ldg(lam_b + nodeidx);
+      scale = __ldg(lam_a + n);
+      mass = __ldg(lam_b + n);
     } else if (PARTIAL) {
-      scale = __ldg(lam_a + nodeidx);
+      scale = __ldg(lam_a + n);
     } else {
       const double dt = fma(fma(det[2], t, det[1]), t, det[0]);
-      const double lam_geo = (0.125 * ((cW<N1>(K) * wj) * wi)) * rcp_fast(dt);
+      const double lam_geo = div_fast(cW<N1>(K) * wji8, dt);  // 0.125 w / det(JT)
       if (HELM) {
-        const double l0 = lam_a ? __ldg(lam_a + nodeidx) : l0v;
-        const double l1 = lam_b ? __ldg(lam_b + nodeidx) : l1v;
+        const double l0 = lam_a ? __ldg(lam_a + n) : l0v;
+        const double l1 = lam_b ? __ldg(lam_b + n) : l1v;
         scale = l0 * lam_geo;
         mass = l1 * (lam_geo * (0.015625 * dt * dt));
       } else {
@@ -184,12 +267,14 @@ struct TrilinearPoly {
 // Stored (Nek-style) factors: 6 (+gwj) SoA loads per node (axlocal.py:181-185).
 template <bool HELM>
 struct StoredLoad {
+  static constexpr bool kStageA = false;
   const double* g;
   const double* gwj;
   const double* lam0;
   const double* lam1;
   double l0v, l1v;
-  __device__ void prepare(const hx_axlocal_args& a, int64_t e, const double*, Fibre) {
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, int64_t e, const TriShared&, const double*, int,
+                                          int) {
     g = a.g + e * 6 * N3;
     gwj = HELM ? a.gwj + e * N3 : nullptr;
     lam0 = a.lam0 ? a.lam0 + e * N3 : nullptr;
@@ -219,16 +304,18 @@ struct StoredLoad {
 // Parallelepiped: w (x) h (geometry.py:389-398).
 template <bool HELM>
 struct Ppd {
+  static constexpr bool kStageA = false;
   double h[7];
   double wj, wi;
   const double* lam0;
   const double* lam1;
   double l0v, l1v;
-  __device__ void prepare(const hx_axlocal_args& a, int64_t e, const double*, Fibre f) {
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, int64_t e, const TriShared&, const double*,
+                                          int fi, int fj) {
 #pragma unroll
     for (int q = 0; q < 7; ++q) h[q] = __ldg(a.h + e * 7 + q);
-    wj = cW<N1>(f.j);
-    wi = cW<N1>(f.i);
+    wj = cW<N1>(fj);
+    wi = cW<N1>(fi);
     lam0 = a.lam0 ? a.lam0 + e * N3 : nullptr;
     lam1 = a.lam1 ? a.lam1 + e * N3 : nullptr;
     l0v = a.lam0_value;
@@ -253,32 +340,58 @@ struct Ppd {
   }
 };
 
-template <typename F, int NCOL, bool HELM, bool NEED_VERTS, int MINB>
-__global__ void __launch_bounds__(64, MINB) ax8(const hx_axlocal_args a) {
-  __shared__ double sX[CUBE];
-  __shared__ double sA[CUBE];
-  __shared__ double sB[CUBE];
-  __shared__ double sV[24];
+template <typename F, int K>
+__device__ __forceinline__ void node_at(const F& fac, int n, double x0, double x1, double x2, double& rr,
+                                        double& ss, double& tt, double& mass) {
+  fac.template node<K>(n, x0, x1, x2, rr, ss, tt, mass);
+}
+
+// Shared memory lives at file scope so that the per-element body can be a
+// separate (non-inlined) function: inlined into the persistent loop, NVVM
+// hoists every __constant__ operand out of the loop into registers and spills.
+// TMA landing zones for x (linear, as in HBM), one per column count
+static __shared__ __align__(128) double s_land1[2][N3];
+static __shared__ __align__(128) double s_land3[2][N3 * 3];
+template <int NCOL>
+__device__ __forceinline__ double* landing(int b) {
+  if constexpr (NCOL == 1)
+    return s_land1[b];
+  else
+    return s_land3[b];
+}
+static __shared__ __align__(16) double s_verts[2][24];  // TMA landing zone for the vertices
+static __shared__ double s_cubeX[CUBE];
+static __shared__ double s_cubeA[CUBE];
+static __shared__ double s_cubeB[CUBE];
+static __shared__ TriShared s_tri;
+static __shared__ __align__(8) uint64_t s_mbar[2];
+
+template <typename F, int NCOL, bool HELM, bool TRI>
+__device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int64_t e, int b) {
+  const hx_axlocal_args& a = *ap;
+  double* sX = s_cubeX;
+  double* sA = s_cubeA;
+  double* sB = s_cubeB;
   const int t = threadIdx.x;
-  const int64_t e = blockIdx.x;
-  // k-fibre (i, j); i-row (j = t&7, k = t>>3); j-column (i = t&7, k = t>>3)
-  const int fi = t & 7, fj = t >> 3;
-  const int kp = Aj(fj) + fi;                  // + Ak(k)
-  const int rb = Ak(t >> 3) + Aj(t & 7);       // + n
-  const int cb = Ak(t >> 3) + (t & 7);         // + Aj(n)
-  if (NEED_VERTS && t < 24) sV[t] = __ldg(a.verts + e * 24 + t);
+  const Roles r = roles(t);
+  const int kp = Aj(r.fj) + r.fi;      // k-fibre base (+ Ak(k))
+  const int rb = Ak(r.rk) + Aj(r.rj);  // i-row base (+ n)
+  const int cb = Ak(r.ck) + r.ci;      // j-column base (+ Aj(n))
+  const int lin = r.fj * 8 + r.fi;     // k-fibre offset in the linear element (+ 64 k)
+  const double* sL = landing<NCOL>(b);
 
 #pragma unroll 1
   for (int c = 0; c < NCOL; ++c) {
     double xk[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) xk[k] = __ldg(a.x + (e * N3 + k * 64 + fj * 8 + fi) * NCOL + c);
+    for (int k = 0; k < 8; ++k) xk[k] = sL[(k * 64 + lin) * NCOL + c];
 #pragma unroll
     for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
+    if (TRI && F::kStageA && c == 0) tri_stage_a(t, s_verts[b], s_tri);
     __syncthreads();
 
     F fac;
-    fac.prepare(a, e, sV, Fibre{fi, fj});
+    fac.prepare(a, e, s_tri, s_verts[b], r.fi, r.fj);
 
     // forward: x2 on the k-fibre; x0 on the i-row; x1 on the j-column
     double x2[8];
@@ -300,23 +413,17 @@ __global__ void __launch_bounds__(64, MINB) ax8(const hx_axlocal_args a) {
 
     // nodewise factor stage on the k-fibre, in place (each address owned by one thread)
     double tt[8], yk[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int adr = Ak(k) + kp;
-      const double x0 = sA[adr], x1 = sB[adr];
-      double rr, ss, mass;
-      switch (k) {
-#define HX_NODE(K) \
-  case K:          \
-    fac.template node<K>(K * 64 + fj * 8 + fi, x0, x1, x2[K], rr, ss, tt[K], mass); \
-    break;
-        HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+#define HX_NODE(K)                                                                  \
+  {                                                                                 \
+    const int adr = Ak(K) + kp;                                                     \
+    double rr, ss, mass;                                                            \
+    node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, tt[K], mass); \
+    sA[adr] = rr;                                                                   \
+    sB[adr] = ss;                                                                   \
+    if (HELM) yk[K] = mass * xk[K];                                                 \
+  }
+    HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
-      }
-      sA[adr] = rr;
-      sB[adr] = ss;
-      yk[k] = HELM ? mass * xk[k] : 0.0;
-    }
     double yt[8];
     eo8<1>(tt, yt);
     __syncthreads();
@@ -337,53 +444,235 @@ __global__ void __launch_bounds__(64, MINB) ax8(const hx_axlocal_args a) {
     }
     __syncthreads();
 
+    double* yout = a.y + e * N3 * NCOL;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int adr = Ak(k) + kp;
-      const double y = (sA[adr] + sB[adr]) + yt[k] + yk[k];
-      a.y[(e * N3 + k * 64 + fj * 8 + fi) * NCOL + c] = y;
+      double y = (sA[adr] + sB[adr]) + yt[k];
+      if (HELM) y += yk[k];
+      yout[(k * 64 + lin) * NCOL + c] = y;
     }
   }
 }
 
-// MINB = resident CTAs per SM the register budget is sized for (64 threads
-// each): 6 -> <= 168 registers, 8 -> <= 128.
-template <typename F, bool HELM, bool NEED_VERTS, int MINB = 6>
-cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
+template <typename F, int NCOL, bool HELM, bool TRI>
+__device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict__ ap, int64_t e) {
+  const int b = 0;
+  const hx_axlocal_args& a = *ap;
+  double* sX = s_cubeX;
+  double* sA = s_cubeA;
+  double* sB = s_cubeB;
+  const int t = threadIdx.x;
+  const Roles r = roles(t);
+  const int kp = Aj(r.fj) + r.fi;      // k-fibre base (+ Ak(k))
+  const int rb = Ak(r.rk) + Aj(r.rj);  // i-row base (+ n)
+  const int cb = Ak(r.ck) + r.ci;      // j-column base (+ Aj(n))
+  const int lin = r.fj * 8 + r.fi;     // k-fibre offset in the linear element (+ 64 k)
+
+#pragma unroll 1
+  for (int c = 0; c < NCOL; ++c) {
+    double xk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xk[k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NCOL + c);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
+    if (TRI && F::kStageA && c == 0) tri_stage_a(t, s_verts[b], s_tri);
+    __syncthreads();
+
+    F fac;
+    fac.prepare(a, e, s_tri, s_verts[b], r.fi, r.fj);
+
+    // forward: x2 on the k-fibre; x0 on the i-row; x1 on the j-column
+    double x2[8];
+    eo8<0>(xk, x2);
+    {
+      double v[8], o[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = sX[rb + n];
+      eo8<0>(v, o);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) sA[rb + n] = o[n];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = sX[cb + Aj(n)];
+      eo8<0>(v, o);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) sB[cb + Aj(n)] = o[n];
+    }
+    __syncthreads();
+
+    // nodewise factor stage on the k-fibre, in place (each address owned by one thread)
+    double tt[8], yk[8];
+#define HX_NODE(K)                                                                  \
+  {                                                                                 \
+    const int adr = Ak(K) + kp;                                                     \
+    double rr, ss, mass;                                                            \
+    node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, tt[K], mass); \
+    sA[adr] = rr;                                                                   \
+    sB[adr] = ss;                                                                   \
+    if (HELM) yk[K] = mass * xk[K];                                                 \
+  }
+    HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+#undef HX_NODE
+    double yt[8];
+    eo8<1>(tt, yt);
+    __syncthreads();
+
+    // transposed: D^T rr on the i-row, D^T ss on the j-column, in place
+    {
+      double v[8], o[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = sA[rb + n];
+      eo8<1>(v, o);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) sA[rb + n] = o[n];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = sB[cb + Aj(n)];
+      eo8<1>(v, o);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) sB[cb + Aj(n)] = o[n];
+    }
+    __syncthreads();
+
+    double* yout = a.y + e * N3 * NCOL;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int adr = Ak(k) + kp;
+      double y = (sA[adr] + sB[adr]) + yt[k];
+      if (HELM) y += yk[k];
+      yout[(k * 64 + lin) * NCOL + c] = y;
+    }
+  }
+}
+
+
+// One CTA per element (no persistent loop): the body inlines into the kernel
+// and D's even-odd blocks stay __constant__ operands.
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
+__global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlocal_args a) {
+  const int64_t e = blockIdx.x;
+  if (TRI && threadIdx.x < 24) s_verts[0][threadIdx.x] = __ldg(a.verts + e * 24 + threadIdx.x);
+  if (TRI) __syncthreads();
+  element_direct<F, NCOL, HELM, TRI>(&a, e);
+}
+
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
+__global__ void __launch_bounds__(64, MINB) ax8(const __grid_constant__ hx_axlocal_args a) {
+  const int t = threadIdx.x;
+  const int64_t E = a.n_elements;
+  constexpr uint32_t kBytes = 4096u * NCOL + (TRI ? 192u : 0u);
+
+  if (t == 0) {
+    mbar_init(&s_mbar[0], 1);
+    mbar_init(&s_mbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t e = blockIdx.x;
+  if (t == 0 && e < E) {
+    mbar_arrive_expect_tx(&s_mbar[0], kBytes);
+    bulk_g2s(landing<NCOL>(0), a.x + e * N3 * NCOL, 4096u * NCOL, &s_mbar[0]);
+    if (TRI) bulk_g2s(s_verts[0], a.verts + e * 24, 192u, &s_mbar[0]);
+  }
+  for (int it = 0; e < E; e += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int64_t en = e + gridDim.x;
+    if (t == 0 && en < E) {
+      // buffer b^1 was last read before the barriers of this CTA's previous element
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&s_mbar[b ^ 1], kBytes);
+      bulk_g2s(landing<NCOL>(b ^ 1), a.x + en * N3 * NCOL, 4096u * NCOL, &s_mbar[b ^ 1]);
+      if (TRI) bulk_g2s(s_verts[b ^ 1], a.verts + en * 24, 192u, &s_mbar[b ^ 1]);
+    }
+    mbar_wait(&s_mbar[b], (it >> 1) & 1);
+    element<F, NCOL, HELM, TRI>(&a, e, b);
+  }
+}
+
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
+cudaError_t launch_n(const hx_axlocal_args& a, cudaStream_t s) {
+  static int grid_cap = 0;  // persistent grid: SMs x resident CTAs (per instantiation)
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess)
+      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax8<F, NCOL, HELM, TRI, MINB>, 64, 0);
+    if (err != cudaSuccess) return err;
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int64_t grid = a.n_elements < grid_cap ? a.n_elements : grid_cap;
+  ax8<F, NCOL, HELM, TRI, MINB><<<(unsigned)grid, 64, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename F, bool HELM, bool TRI, int MINB>
+cudaError_t launch_single(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)a.n_elements;
   if (a.n_col == 3)
-    ax8<F, 3, HELM, NEED_VERTS, MINB><<<grid, 64, 0, s>>>(a);
+    ax8s<F, 3, HELM, TRI, MINB><<<grid, 64, 0, s>>>(a);
   else
-    ax8<F, 1, HELM, NEED_VERTS, MINB><<<grid, 64, 0, s>>>(a);
+    ax8s<F, 1, HELM, TRI, MINB><<<grid, 64, 0, s>>>(a);
   return cudaGetLastError();
 }
+
+// MINB = resident 64-thread CTAs per SM the register budget is sized for
+// (8 -> <= 128 registers, 6 -> <= 168).
+template <typename F, bool HELM, bool TRI, int MINB = 8>
+cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
+  if (a.n_col == 3) return launch_n<F, 3, HELM, TRI, MINB>(a, s);
+  return launch_n<F, 1, HELM, TRI, MINB>(a, s);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace fast
 }  // namespace hx
 
+// Kernel choice per variant (measured on B200, tools/sweep.py, profiles/):
+//  * trilinear family (FP64-bound): one CTA per element (ax8s), shared
+//    per-element setup, 8 CTAs/SM;
+//  * stored / parallelepiped (HBM-bound): also one CTA per element — with
+//    8 CTAs/SM the plain coalesced loads reach 7.0 TB/s, ahead of the
+//    persistent TMA-prefetch pipeline (ax8, hook 1: 6.6 TB/s).
+// `reserved` is a tuning hook used by tools/sweep.py to time the alternatives.
 extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) {
   using namespace hx::fast;
   if (a->order != 7) return cudaErrorNotSupported;
+  // the bulk copies need 16-byte aligned sources
+  if (!aligned16(a->x) || (a->verts && !aligned16(a->verts))) return cudaErrorNotSupported;
   const bool helm = a->equation == HX_HELMHOLTZ;
+  const int hook = a->reserved;
   switch (a->factor_source) {
     case HX_TRILINEAR:
-      if (helm) return launch<TrilinearPoly<true, false, false>, true, true>(*a, s);
-      // tuning hook (reserved != 0): alternative register budgets
-      switch (a->reserved) {
-        case 4: return launch<TrilinearPoly<false, false, false>, false, true, 4>(*a, s);
-        case 5: return launch<TrilinearPoly<false, false, false>, false, true, 5>(*a, s);
-        case 8: return launch<TrilinearPoly<false, false, false>, false, true, 8>(*a, s);
-        default: return launch<TrilinearPoly<false, false, false>, false, true>(*a, s);
+      if (helm) {
+        if (hook == 1) return launch<TrilinearPoly<true, false, false>, true, true>(*a, s);
+        return launch_single<TrilinearPoly<true, false, false>, true, true, 8>(*a, s);
+      }
+      switch (hook) {
+        case 1: return launch<TrilinearPoly<false, false, false>, false, true>(*a, s);
+        case 6: return launch<TrilinearPoly<false, false, false>, false, true, 6>(*a, s);
+        case 9: return launch<TrilinearPoly<false, false, false, false>, false, true, 6>(*a, s);
+        case 10: return launch_single<TrilinearPoly<false, false, false, true>, false, true, 6>(*a, s);
+        case 11: return launch_single<TrilinearPoly<false, false, false, false>, false, true, 6>(*a, s);
+        case 13: return launch_single<TrilinearPoly<false, false, false, false>, false, true, 8>(*a, s);
+        default: return launch_single<TrilinearPoly<false, false, false, true>, false, true, 8>(*a, s);
       }
     case HX_TRILINEAR_PARTIAL:
-      return launch<TrilinearPoly<false, false, true>, false, true>(*a, s);
+      if (hook == 1) return launch<TrilinearPoly<false, false, true>, false, true>(*a, s);
+      return launch_single<TrilinearPoly<false, false, true>, false, true, 8>(*a, s);
     case HX_TRILINEAR_MERGED:
-      return launch<TrilinearPoly<true, true, false>, true, true>(*a, s);
+      if (hook == 1) return launch<TrilinearPoly<true, true, false>, true, true>(*a, s);
+      return launch_single<TrilinearPoly<true, true, false>, true, true, 8>(*a, s);
     case HX_STORED:
-      return helm ? launch<StoredLoad<true>, true, false>(*a, s) : launch<StoredLoad<false>, false, false>(*a, s);
+      if (hook == 1)
+        return helm ? launch<StoredLoad<true>, true, false>(*a, s) : launch<StoredLoad<false>, false, false>(*a, s);
+      return helm ? launch_single<StoredLoad<true>, true, false, 8>(*a, s)
+                  : launch_single<StoredLoad<false>, false, false, 8>(*a, s);
     case HX_PARALLELEPIPED:
-      return helm ? launch<Ppd<true>, true, false>(*a, s) : launch<Ppd<false>, false, false>(*a, s);
+      if (hook == 1)
+        return helm ? launch<Ppd<true>, true, false>(*a, s) : launch<Ppd<false>, false, false>(*a, s);
+      return helm ? launch_single<Ppd<true>, true, false, 8>(*a, s) : launch_single<Ppd<false>, false, false, 8>(*a, s);
   }
   return cudaErrorNotSupported;
 }
@@ -396,10 +685,10 @@ extern "C" cudaError_t hx_upload_basis_fast(int n1, const double* pts, const dou
   for (int T = 0; T < 2; ++T)
     for (int i = 0; i < 4; ++i)
       for (int m = 0; m < 4; ++m) {
-        const double a = T ? d[m * 8 + i] : d[i * 8 + m];            // M[i][m]
-        const double b = T ? d[(7 - m) * 8 + i] : d[i * 8 + 7 - m];  // M[i][7-m]
-        eo[T][0][i][m] = 0.5 * (a + b);
-        eo[T][1][i][m] = 0.5 * (a - b);
+        const double x = T ? d[m * 8 + i] : d[i * 8 + m];            // M[i][m]
+        const double y = T ? d[(7 - m) * 8 + i] : d[i * 8 + 7 - m];  // M[i][7-m]
+        eo[T][0][i][m] = 0.5 * (x + y);
+        eo[T][1][i][m] = 0.5 * (x - y);
       }
   return cudaMemcpyToSymbol(c_EO, eo, sizeof(eo));
 }

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--only", default=None)
+    ap.add_argument("--hook", type=int, default=None, help="run only this tuning hook")
     args = ap.parse_args()
     ex, ey, ez = (int(v) for v in args.mesh.split(","))
     order = args.order
@@ -37,20 +38,28 @@ def main():
     rows = []
     cases = [
         ("poisson", 1, "trilinear", 0, 0),
-        ("poisson", 1, "trilinear", 0, 4),
-        ("poisson", 1, "trilinear", 0, 5),
-        ("poisson", 1, "trilinear", 0, 8),
+        ("poisson", 1, "trilinear", 0, 1),
+        ("poisson", 1, "trilinear", 0, 13),
         ("poisson", 1, "trilinear", 1, 0),
         ("poisson", 1, "trilinear-partial", 0, 0),
+        ("poisson", 1, "trilinear-partial", 0, 1),
         ("poisson", 1, "stored", 0, 0),
+        ("poisson", 1, "stored", 0, 2),
         ("poisson", 1, "stored", 1, 0),
         ("poisson", 1, "parallelepiped", 0, 0),
+        ("poisson", 1, "parallelepiped", 0, 2),
         ("helmholtz", 1, "trilinear", 0, 0),
+        ("helmholtz", 1, "trilinear", 0, 1),
         ("helmholtz", 1, "trilinear-merged", 0, 0),
+        ("helmholtz", 1, "trilinear-merged", 0, 1),
+        ("helmholtz", 1, "stored", 0, 0),
         ("poisson", 3, "trilinear", 0, 0),
+        ("poisson", 3, "stored", 0, 0),
     ]
     for eq, ncol, src, kernel, hook in cases:
         if args.only and args.only not in src:
+            continue
+        if args.hook is not None and (hook != args.hook or kernel != 0):
             continue
         spec = hx.KernelSpec(eq, ncol, src, order)
         v = verts_ppd if src == "parallelepiped" else verts
