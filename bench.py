@@ -59,45 +59,26 @@ def parse():
     return p.parse_args()
 
 
-# --------------------------------------------------------------------------
-# distributed plumbing
-class World:
-    def __init__(self):
-        self.size = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
+from paper_2504_07042_b200.sharding import World, slab_layers  # noqa: E402
 
-    def init(self, backend):
-        if self.size > 1:
-            import torch.distributed as dist
-
-            dist.init_process_group(backend=backend)
-            self.pg = dist
-
-    def barrier(self):
-        if self.pg:
-            self.pg.barrier()
-
-    def max(self, value: float, device) -> float:
-        if not self.pg:
-            return value
-        import torch
-
-        t = torch.tensor([value], dtype=torch.float64, device=device)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
-        return float(t.item())
-
-    def close(self):
-        if self.pg:
-            self.pg.destroy_process_group()
+TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
 def slab(world: World, ez: int):
-    if ez % world.size:
-        raise SystemExit(f"{ez} z-layers do not divide over {world.size} ranks")
-    per = ez // world.size
-    return world.rank * per, (world.rank + 1) * per
+    return slab_layers(ez, world.size, world.rank)
+
+
+def measured_traffic(kernel_key: str, elements_per_gpu: int):
+    """DRAM bytes per launch from the committed ncu --set full capture, if it
+    was taken on this exact per-GPU workload."""
+    try:
+        with open(TRAFFIC) as fh:
+            rec = json.load(fh)[kernel_key]
+    except Exception:
+        return None, None
+    if rec.get("elements_per_gpu") != elements_per_gpu:
+        return None, None
+    return rec["dram_bytes_per_launch"], rec["source"]
 
 
 # --------------------------------------------------------------------------
@@ -342,6 +323,7 @@ def hx_arm(args, world):
         return out
 
     main = measure("trilinear", with_clocks=True)
+    traffic, traffic_src = measured_traffic("trilinear", E)
     result = {
         "metric": METRIC,
         "value": main["gdofs"],
@@ -372,7 +354,8 @@ def hx_arm(args, world):
             "peak": fp64_peak,
             "unit": "TFLOP/s",
             "frac": main["tflops"] / fp64_peak,
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": "measured FP64 DFMA/DMMA peak on this pool (tools/ubench_fp64.cu, "
             "profiles/r01_ubench_fp64.txt); MEASURED_PEAKS.json has no fp64 entry",
             "algorithmic_flops_per_element": 56832 + 44416,
