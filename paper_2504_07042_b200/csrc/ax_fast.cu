@@ -34,6 +34,7 @@ namespace fast {
 constexpr int N1 = 8;
 constexpr int N3 = 512;
 constexpr int CUBE = 544;  // 543 used
+constexpr int64_t kPrefetchAhead = 2368;  // two waves of 148 SMs x 8 CTAs
 
 __host__ __device__ constexpr int Aj(int j) { return 17 * (j >> 1) + 8 * (j & 1); }
 __host__ __device__ constexpr int Ak(int k) { return 68 * k; }
@@ -62,13 +63,26 @@ __device__ __forceinline__ Roles roles(int t) {
 
 // Even-odd blocks: [0] forward D, [1] transposed D^T; [.][0] = A (even), [.][1] = B (odd);
 // A[i][m] = (M[i][m] + M[i][7-m]) / 2, B[i][m] = (M[i][m] - M[i][7-m]) / 2 for M = D or D^T.
-static __constant__ double c_EO[2][2][4][4];
+// [copy]: two identical copies so that code for the two fibre roles of the
+// warp-per-element kernel does not share (and keep live) the same constants.
+static __constant__ double c_EO[2][2][2][4][4];
 
 namespace hx {
 namespace fast {
 
+// Basis value at a thread-dependent index: eight uniform constant loads and a
+// select chain instead of a divergent indexed LDC (which serialises per lane).
+__device__ __forceinline__ double pick8(const double* c, int idx) {
+  double v = c[0];
+#pragma unroll
+  for (int q = 1; q < 8; ++q) v = idx == q ? c[q] : v;
+  return v;
+}
+__device__ __forceinline__ double xr(int idx) { return pick8(c_X + off_p(N1), idx); }
+__device__ __forceinline__ double wr(int idx) { return pick8(c_W + off_p(N1), idx); }
+
 // out = M v for an 8-point fibre, M = D (T=0) or D^T (T=1).
-template <int T>
+template <int T, int COPY = 0>
 __device__ __forceinline__ void eo8(const double v[8], double out[8]) {
   double ue[4], uo[4];
 #pragma unroll
@@ -78,12 +92,12 @@ __device__ __forceinline__ void eo8(const double v[8], double out[8]) {
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double p = c_EO[T][0][i][0] * ue[0];
-    double q = c_EO[T][1][i][0] * uo[0];
+    double p = c_EO[COPY][T][0][i][0] * ue[0];
+    double q = c_EO[COPY][T][1][i][0] * uo[0];
 #pragma unroll
     for (int m = 1; m < 4; ++m) {
-      p = fma(c_EO[T][0][i][m], ue[m], p);
-      q = fma(c_EO[T][1][i][m], uo[m], q);
+      p = fma(c_EO[COPY][T][0][i][m], ue[m], p);
+      q = fma(c_EO[COPY][T][1][i][m], uo[m], q);
     }
     out[i] = p + q;
     out[7 - i] = q - p;
@@ -104,6 +118,8 @@ struct TriShared {
   double j[8][6];  // dr_base[3], dr_slope[3] per j
   double i[8][6];  // ds_base[3], ds_slope[3] per i
   double d[12];     // v4-v0, v5-v1, v7-v3, v6-v2
+  double t00[8][9];  // K00(j, k): depends on j and k only (padded rows)
+  double t11[8][9];  // K11(i, k): depends on i and k only
 };
 
 __device__ __forceinline__ double dot3(const double* u, const double* v) {
@@ -118,7 +134,7 @@ __device__ __forceinline__ void tri_stage_a(int t, const double* __restrict__ v,
     const bool jside = t < 24;
     const int task = jside ? t : t - 24;
     const int idx = task / 3, c = task % 3;
-    const double xi = cX<N1>(idx);
+    const double xi = xr(idx);
     const double a0 = 1.0 - xi, a1 = 1.0 + xi;
     // j side: tmp1 = a0 (v1-v0) + a1 (v3-v2), tmp2 = a0 (v5-v4) + a1 (v7-v6)
     // i side: tmp3 = a0 (v2-v0) + a1 (v3-v1), tmp4 = a0 (v6-v4) + a1 (v7-v5)
@@ -142,10 +158,17 @@ __device__ __forceinline__ void tri_stage_a(int t, const double* __restrict__ v,
 // node<K>(...) per node of the k-fibre.
 
 // Trilinear recompute (geometry.py:304-351; axlocal.py:191-211), polynomial in t.
-template <bool HELM, bool MERGED, bool PARTIAL, bool SHARED = true>
+template <bool HELM, bool MERGED, bool PARTIAL, bool SHARED = true, bool LAMFIRST = false, bool TTSMEM = false,
+          bool TAB = false>
 struct TrilinearPoly {
   static constexpr bool kStageA = SHARED;
+  static constexpr bool kScaleFirst = LAMFIRST;
+  static constexpr bool kTtSmem = TTSMEM;
+  // TAB: K00(j,k) and K11(i,k) are evaluated once per element into shared
+  // tables (each thread fills one entry of each) instead of per fibre node.
   double k00[3], k11[3], k01[3], k02[2], k12[2], k22, det[3];
+  const double* tab00;  // &t00[fj][0]
+  const double* tab11;  // &t11[fi][0]
   double wji8;
   const double* lam_a;  // partial: lam_geo; merged: lam2; trilinear-helm: lam0 (or null)
   const double* lam_b;  // merged: lam3; trilinear-helm: lam1 (or null)
@@ -154,6 +177,8 @@ struct TrilinearPoly {
   __device__ __forceinline__ void prepare(const hx_axlocal_args& a, int64_t e, const TriShared& s,
                                           const double* sv, int fi, int fj) {
     double br[3], sr[3], bs[3], ss[3], c[3];
+    tab00 = s.t00[fj];
+    tab11 = s.t11[fi];
     if (SHARED) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -164,7 +189,7 @@ struct TrilinearPoly {
       }
     } else {
       TrilinearPencil p;
-      trilinear_pencil(sv, cX<N1>(fi), cX<N1>(fj), p);
+      trilinear_pencil(sv, xr(fi), xr(fj), p);
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         br[q] = p.dr_base[q];
@@ -173,20 +198,34 @@ struct TrilinearPoly {
         ss[q] = p.ds_slope[q];
       }
     }
-    k00[0] = dot3(br, br);
-    k00[1] = 2.0 * dot3(br, sr);
-    k00[2] = dot3(sr, sr);
-    k11[0] = dot3(bs, bs);
-    k11[1] = 2.0 * dot3(bs, ss);
-    k11[2] = dot3(ss, ss);
+    if (TAB) {
+      // this thread's entries: K00(j = fj, k = fi) and K11(i = fi, k = fj)
+      TriShared& w = const_cast<TriShared&>(s);
+      const double tk = xr(fi), tj = xr(fj);
+      double cr[3], cs[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        cr[q] = br[q] + tk * sr[q];
+        cs[q] = bs[q] + tj * ss[q];
+      }
+      w.t00[fj][fi] = dot3(cr, cr);
+      w.t11[fi][fj] = dot3(cs, cs);
+    } else {
+      k00[0] = dot3(br, br);
+      k00[1] = 2.0 * dot3(br, sr);
+      k00[2] = dot3(sr, sr);
+      k11[0] = dot3(bs, bs);
+      k11[1] = 2.0 * dot3(bs, ss);
+      k11[2] = dot3(ss, ss);
+    }
     if (SHARED) {
-      const double xj = cX<N1>(fj), xi = cX<N1>(fi);
+      const double xj = xr(fj), xi = xr(fi);
       const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
       const double w00 = a0j * a0i, w01 = a0j * a1i, w10 = a1j * a0i, w11 = a1j * a1i;
 #pragma unroll
       for (int q = 0; q < 3; ++q) c[q] = w00 * s.d[q] + w01 * s.d[3 + q] + w11 * s.d[6 + q] + w10 * s.d[9 + q];
     } else {
-      const double xj = cX<N1>(fj), xi = cX<N1>(fi);
+      const double xj = xr(fj), xi = xr(fi);
       const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
       const double w00 = a0j * a0i, w01 = a0j * a1i, w10 = a1j * a0i, w11 = a1j * a1i;
 #pragma unroll
@@ -208,7 +247,7 @@ struct TrilinearPoly {
     det[0] = dot3(br, P);
     det[1] = dot3(br, Q) + dot3(sr, P);
     det[2] = dot3(sr, Q);
-    wji8 = 0.125 * (cW<N1>(fj) * cW<N1>(fi));
+    wji8 = 0.125 * (wr(fj) * wr(fi));
     lam_a = lam_b = nullptr;
     l0v = a.lam0_value;
     l1v = a.lam1_value;
@@ -223,22 +262,10 @@ struct TrilinearPoly {
     }
   }
 
+  // Per-node scale (grad_scale) and mass coefficient; independent of x.
   template <int K>
-  __device__ __forceinline__ void node(int n, double x0, double x1, double x2, double& rr, double& ss, double& tt,
-                                       double& mass) const {
+  __device__ __forceinline__ void scale_at(int n, double& scale, double& mass) const {
     const double t = cX<N1>(K);
-    const double a00 = fma(fma(k00[2], t, k00[1]), t, k00[0]);
-    const double a11 = fma(fma(k11[2], t, k11[1]), t, k11[0]);
-    const double a01 = fma(fma(k01[2], t, k01[1]), t, k01[0]);
-    const double a02 = fma(k02[1], t, k02[0]);
-    const double a12 = fma(k12[1], t, k12[0]);
-    const double g0 = fma(a11, k22, -a12 * a12);
-    const double g1 = fma(a02, a12, -a01 * k22);
-    const double g2 = fma(a01, a12, -a02 * a11);
-    const double g3 = fma(a00, k22, -a02 * a02);
-    const double g4 = fma(a01, a02, -a00 * a12);
-    const double g5 = fma(a00, a11, -a01 * a01);
-    double scale;
     mass = 0.0;
     if (MERGED) {
       scale = __ldg(lam_a + n);
@@ -257,10 +284,36 @@ struct TrilinearPoly {
         scale = lam_geo;
       }
     }
+  }
+
+  // rr, ss, tt = scale * adj(K(t_K)) (x0, x1, x2).
+  template <int K>
+  __device__ __forceinline__ void apply_at(double scale, double x0, double x1, double x2, double& rr, double& ss,
+                                           double& tt) const {
+    const double t = cX<N1>(K);
+    const double a00 = TAB ? tab00[K] : fma(fma(k00[2], t, k00[1]), t, k00[0]);
+    const double a11 = TAB ? tab11[K] : fma(fma(k11[2], t, k11[1]), t, k11[0]);
+    const double a01 = fma(fma(k01[2], t, k01[1]), t, k01[0]);
+    const double a02 = fma(k02[1], t, k02[0]);
+    const double a12 = fma(k12[1], t, k12[0]);
+    const double g0 = fma(a11, k22, -a12 * a12);
+    const double g1 = fma(a02, a12, -a01 * k22);
+    const double g2 = fma(a01, a12, -a02 * a11);
+    const double g3 = fma(a00, k22, -a02 * a02);
+    const double g4 = fma(a01, a02, -a00 * a12);
+    const double g5 = fma(a00, a11, -a01 * a01);
     const double s0 = scale * x0, s1 = scale * x1, s2 = scale * x2;
     rr = fma(g0, s0, fma(g1, s1, g2 * s2));
     ss = fma(g1, s0, fma(g3, s1, g4 * s2));
     tt = fma(g2, s0, fma(g4, s1, g5 * s2));
+  }
+
+  template <int K>
+  __device__ __forceinline__ void node(int n, double x0, double x1, double x2, double& rr, double& ss, double& tt,
+                                       double& mass) const {
+    double scale;
+    scale_at<K>(n, scale, mass);
+    apply_at<K>(scale, x0, x1, x2, rr, ss, tt);
   }
 };
 
@@ -268,6 +321,8 @@ struct TrilinearPoly {
 template <bool HELM>
 struct StoredLoad {
   static constexpr bool kStageA = false;
+  static constexpr bool kScaleFirst = false;
+  static constexpr bool kTtSmem = false;
   const double* g;
   const double* gwj;
   const double* lam0;
@@ -305,6 +360,8 @@ struct StoredLoad {
 template <bool HELM>
 struct Ppd {
   static constexpr bool kStageA = false;
+  static constexpr bool kScaleFirst = false;
+  static constexpr bool kTtSmem = false;
   double h[7];
   double wj, wi;
   const double* lam0;
@@ -314,8 +371,8 @@ struct Ppd {
                                           int fi, int fj) {
 #pragma unroll
     for (int q = 0; q < 7; ++q) h[q] = __ldg(a.h + e * 7 + q);
-    wj = cW<N1>(fj);
-    wi = cW<N1>(fi);
+    wj = wr(fj);
+    wi = wr(fi);
     lam0 = a.lam0 ? a.lam0 + e * N3 : nullptr;
     lam1 = a.lam1 ? a.lam1 + e * N3 : nullptr;
     l0v = a.lam0_value;
@@ -352,6 +409,15 @@ __device__ __forceinline__ void node_at(const F& fac, int n, double x0, double x
 // TMA landing zones for x (linear, as in HBM), one per column count
 static __shared__ __align__(128) double s_land1[2][N3];
 static __shared__ __align__(128) double s_land3[2][N3 * 3];
+static __shared__ __align__(128) double s_land1_one[N3];
+static __shared__ __align__(128) double s_land3_one[N3 * 3];
+template <int NCOL>
+__device__ __forceinline__ double* landing_one() {
+  if constexpr (NCOL == 1)
+    return s_land1_one;
+  else
+    return s_land3_one;
+}
 template <int NCOL>
 __device__ __forceinline__ double* landing(int b) {
   if constexpr (NCOL == 1)
@@ -413,6 +479,24 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
 
     // nodewise factor stage on the k-fibre, in place (each address owned by one thread)
     double tt[8], yk[8];
+    if constexpr (F::kScaleFirst) {
+      // all eight reciprocals first: eight independent chains for the scheduler
+      double sc[8], ms[8];
+#define HX_SCALE(K) fac.template scale_at<K>(K * 64 + lin, sc[K], ms[K]);
+      HX_SCALE(0) HX_SCALE(1) HX_SCALE(2) HX_SCALE(3) HX_SCALE(4) HX_SCALE(5) HX_SCALE(6) HX_SCALE(7)
+#undef HX_SCALE
+#define HX_NODE(K)                                                          \
+  {                                                                         \
+    const int adr = Ak(K) + kp;                                             \
+    double rr, ss;                                                          \
+    fac.template apply_at<K>(sc[K], sA[adr], sB[adr], x2[K], rr, ss, tt[K]); \
+    sA[adr] = rr;                                                           \
+    sB[adr] = ss;                                                           \
+    if (HELM) yk[K] = ms[K] * xk[K];                                        \
+  }
+      HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+#undef HX_NODE
+    } else {
 #define HX_NODE(K)                                                                  \
   {                                                                                 \
     const int adr = Ak(K) + kp;                                                     \
@@ -422,8 +506,9 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
     sB[adr] = ss;                                                                   \
     if (HELM) yk[K] = mass * xk[K];                                                 \
   }
-    HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+      HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
+    }
     double yt[8];
     eo8<1>(tt, yt);
     __syncthreads();
@@ -455,9 +540,10 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
   }
 }
 
-template <typename F, int NCOL, bool HELM, bool TRI>
-__device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict__ ap, int64_t e) {
-  const int b = 0;
+// COPY selects the copy of the D blocks (so two bodies in one kernel do not
+// share constants); XLAND reads x from the single-element TMA landing buffer.
+template <typename F, int NCOL, bool HELM, bool TRI, int COPY = 0, bool XLAND = false>
+__device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict__ ap, int64_t e, int b = 0) {
   const hx_axlocal_args& a = *ap;
   double* sX = s_cubeX;
   double* sA = s_cubeA;
@@ -473,7 +559,8 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
   for (int c = 0; c < NCOL; ++c) {
     double xk[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) xk[k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NCOL + c);
+    for (int k = 0; k < 8; ++k)
+      xk[k] = XLAND ? landing_one<NCOL>()[(k * 64 + lin) * NCOL + c] : __ldg(a.x + (e * N3 + k * 64 + lin) * NCOL + c);
 #pragma unroll
     for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
     if (TRI && F::kStageA && c == 0) tri_stage_a(t, s_verts[b], s_tri);
@@ -484,17 +571,17 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
 
     // forward: x2 on the k-fibre; x0 on the i-row; x1 on the j-column
     double x2[8];
-    eo8<0>(xk, x2);
+    eo8<0, COPY>(xk, x2);
     {
       double v[8], o[8];
 #pragma unroll
       for (int n = 0; n < 8; ++n) v[n] = sX[rb + n];
-      eo8<0>(v, o);
+      eo8<0, COPY>(v, o);
 #pragma unroll
       for (int n = 0; n < 8; ++n) sA[rb + n] = o[n];
 #pragma unroll
       for (int n = 0; n < 8; ++n) v[n] = sX[cb + Aj(n)];
-      eo8<0>(v, o);
+      eo8<0, COPY>(v, o);
 #pragma unroll
       for (int n = 0; n < 8; ++n) sB[cb + Aj(n)] = o[n];
     }
@@ -502,6 +589,39 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
 
     // nodewise factor stage on the k-fibre, in place (each address owned by one thread)
     double tt[8], yk[8];
+    if constexpr (F::kScaleFirst) {
+      // all eight reciprocals first: eight independent chains for the scheduler
+      double sc[8], ms[8];
+#define HX_SCALE(K) fac.template scale_at<K>(K * 64 + lin, sc[K], ms[K]);
+      HX_SCALE(0) HX_SCALE(1) HX_SCALE(2) HX_SCALE(3) HX_SCALE(4) HX_SCALE(5) HX_SCALE(6) HX_SCALE(7)
+#undef HX_SCALE
+#define HX_NODE(K)                                                          \
+  {                                                                         \
+    const int adr = Ak(K) + kp;                                             \
+    double rr, ss;                                                          \
+    fac.template apply_at<K>(sc[K], sA[adr], sB[adr], x2[K], rr, ss, tt[K]); \
+    sA[adr] = rr;                                                           \
+    sB[adr] = ss;                                                           \
+    if (HELM) yk[K] = ms[K] * xk[K];                                        \
+  }
+      HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+#undef HX_NODE
+    } else if constexpr (F::kTtSmem && !HELM) {
+      // park each tt in the (consumed) x cube instead of holding 8 registers
+#define HX_NODE(K)                                                                   \
+  {                                                                                  \
+    const int adr = Ak(K) + kp;                                                      \
+    double rr, ss, t_, mass;                                                         \
+    node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, t_, mass);     \
+    sA[adr] = rr;                                                                    \
+    sB[adr] = ss;                                                                    \
+    sX[adr] = t_;                                                                    \
+  }
+      HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+#undef HX_NODE
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tt[k] = sX[Ak(k) + kp];
+    } else {
 #define HX_NODE(K)                                                                  \
   {                                                                                 \
     const int adr = Ak(K) + kp;                                                     \
@@ -511,10 +631,11 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
     sB[adr] = ss;                                                                   \
     if (HELM) yk[K] = mass * xk[K];                                                 \
   }
-    HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+      HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
+    }
     double yt[8];
-    eo8<1>(tt, yt);
+    eo8<1, COPY>(tt, yt);
     __syncthreads();
 
     // transposed: D^T rr on the i-row, D^T ss on the j-column, in place
@@ -522,12 +643,12 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
       double v[8], o[8];
 #pragma unroll
       for (int n = 0; n < 8; ++n) v[n] = sA[rb + n];
-      eo8<1>(v, o);
+      eo8<1, COPY>(v, o);
 #pragma unroll
       for (int n = 0; n < 8; ++n) sA[rb + n] = o[n];
 #pragma unroll
       for (int n = 0; n < 8; ++n) v[n] = sB[cb + Aj(n)];
-      eo8<1>(v, o);
+      eo8<1, COPY>(v, o);
 #pragma unroll
       for (int n = 0; n < 8; ++n) sB[cb + Aj(n)] = o[n];
     }
@@ -550,9 +671,56 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
 template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
 __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlocal_args a) {
   const int64_t e = blockIdx.x;
+  // CTAs start in blockIdx order, ~148 x 8 resident at a time: warm L2 for the
+  // element two waves ahead so its CTA's loads do not wait on HBM latency.
+  if (a.reserved != 3 && threadIdx.x == 0) {
+    const int64_t ahead = e + kPrefetchAhead;
+    if (ahead < a.n_elements) {
+      bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
+      if (TRI) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
+    }
+  }
   if (TRI && threadIdx.x < 24) s_verts[0][threadIdx.x] = __ldg(a.verts + e * 24 + threadIdx.x);
   if (TRI) __syncthreads();
   element_direct<F, NCOL, HELM, TRI>(&a, e);
+}
+
+// Two elements per CTA in straight-line code: the second element's x and
+// vertices arrive by TMA bulk copy while the first is computed, so half of the
+// CTA-start load latency disappears without a loop (a loop lets NVVM hoist the
+// D-block constants into registers; see element()).
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
+__global__ void __launch_bounds__(64, MINB) ax8d(const __grid_constant__ hx_axlocal_args a) {
+  const int64_t e0 = 2 * (int64_t)blockIdx.x, e1 = e0 + 1;
+  const bool has1 = e1 < a.n_elements;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    mbar_init(&s_mbar[1], 1);
+    fence_mbar_init();
+  }
+  if (TRI && t < 24) s_verts[0][t] = __ldg(a.verts + e0 * 24 + t);
+  __syncthreads();
+  if (t == 0 && has1) {
+    mbar_arrive_expect_tx(&s_mbar[1], 4096u * NCOL + (TRI ? 192u : 0u));
+    bulk_g2s(landing_one<NCOL>(), a.x + e1 * N3 * NCOL, 4096u * NCOL, &s_mbar[1]);
+    if (TRI) bulk_g2s(s_verts[1], a.verts + e1 * 24, 192u, &s_mbar[1]);
+  }
+  element_direct<F, NCOL, HELM, TRI, 0, false>(&a, e0, 0);
+  if (has1) {
+    mbar_wait(&s_mbar[1], 0);
+    element_direct<F, NCOL, HELM, TRI, 1, true>(&a, e1, 1);
+  }
+}
+
+template <typename F, bool HELM, bool TRI, int MINB>
+cudaError_t launch_double(const hx_axlocal_args& a, cudaStream_t s) {
+  const int64_t blocks = (a.n_elements + 1) / 2;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  if (a.n_col == 3)
+    ax8d<F, 3, HELM, TRI, MINB><<<(unsigned)blocks, 64, 0, s>>>(a);
+  else
+    ax8d<F, 1, HELM, TRI, MINB><<<(unsigned)blocks, 64, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
@@ -586,6 +754,124 @@ __global__ void __launch_bounds__(64, MINB) ax8(const __grid_constant__ hx_axloc
     mbar_wait(&s_mbar[b], (it >> 1) & 1);
     element<F, NCOL, HELM, TRI>(&a, e, b);
   }
+}
+
+// One element per WARP (32-thread CTA): each lane plays two fibre roles
+// (t = lane and t = 32 + lane of the 64-role maps above), phases are separated
+// by __syncwarp only, and no register state crosses a phase: x2 is recomputed
+// from the x fibre in the node phase and the t-transpose result is parked in
+// place of x in the X cube.  The node phase of one role is an out-of-line
+// function so that the two roles cannot share (and keep live) constants.
+template <typename F, bool HELM, int COPY>
+__device__ __noinline__ void warp_node_phase(const hx_axlocal_args* __restrict__ ap, int64_t e, int role) {
+  const hx_axlocal_args& a = *ap;
+  double* sX = s_cubeX;
+  double* sA = s_cubeA;
+  double* sB = s_cubeB;
+  const Roles r = roles(role);
+  const int kp = Aj(r.fj) + r.fi, lin = r.fj * 8 + r.fi;
+  F fac;
+  fac.prepare(a, e, s_tri, s_verts[0], r.fi, r.fj);
+  double xk[8], x2[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) xk[k] = sX[Ak(k) + kp];
+  eo8<0, COPY>(xk, x2);
+  double tt[8], yk[8];
+#define HX_NODE(K)                                                                  \
+  {                                                                                 \
+    const int adr = Ak(K) + kp;                                                     \
+    double rr, ss, mass;                                                            \
+    node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, tt[K], mass); \
+    sA[adr] = rr;                                                                   \
+    sB[adr] = ss;                                                                   \
+    if (HELM) yk[K] = mass * xk[K];                                                 \
+  }
+  HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
+#undef HX_NODE
+  double yt[8];
+  eo8<1, COPY>(tt, yt);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = HELM ? yt[k] + yk[k] : yt[k];
+}
+
+template <int T, int COPY>
+__device__ __forceinline__ void warp_rowcol(int role, double* sR, double* sC, const double* srcR,
+                                            const double* srcC) {
+  const Roles r = roles(role);
+  const int rb = Ak(r.rk) + Aj(r.rj), cb = Ak(r.ck) + r.ci;
+  double v[8], o[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) v[n] = srcR[rb + n];
+  eo8<T, COPY>(v, o);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) sR[rb + n] = o[n];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) v[n] = srcC[cb + Aj(n)];
+  eo8<T, COPY>(v, o);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) sC[cb + Aj(n)] = o[n];
+}
+
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
+__global__ void __launch_bounds__(32, MINB) ax8w(const __grid_constant__ hx_axlocal_args a) {
+  double* sX = s_cubeX;
+  double* sA = s_cubeA;
+  double* sB = s_cubeB;
+  const int lane = threadIdx.x;
+  const int64_t e = blockIdx.x;
+  if (TRI && lane < 24) s_verts[0][lane] = __ldg(a.verts + e * 24 + lane);
+  if (TRI) __syncwarp();
+
+#pragma unroll 1
+  for (int c = 0; c < NCOL; ++c) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const Roles r = roles(32 * p + lane);
+      const int kp = Aj(r.fj) + r.fi, lin = r.fj * 8 + r.fi;
+      double xk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xk[k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NCOL + c);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
+    }
+    if (TRI && F::kStageA && c == 0) {
+      tri_stage_a(lane, s_verts[0], s_tri);
+      tri_stage_a(lane + 32, s_verts[0], s_tri);
+    }
+    __syncwarp();
+    warp_rowcol<0, 0>(lane, sA, sB, sX, sX);
+    warp_rowcol<0, 1>(32 + lane, sA, sB, sX, sX);
+    __syncwarp();
+    warp_node_phase<F, HELM, 0>(&a, e, lane);
+    warp_node_phase<F, HELM, 1>(&a, e, 32 + lane);
+    __syncwarp();
+    warp_rowcol<1, 0>(lane, sA, sB, sA, sB);
+    warp_rowcol<1, 1>(32 + lane, sA, sB, sA, sB);
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const Roles r = roles(32 * p + lane);
+      const int kp = Aj(r.fj) + r.fi, lin = r.fj * 8 + r.fi;
+      double* yout = a.y + e * N3 * NCOL;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int adr = Ak(k) + kp;
+        yout[(k * 64 + lin) * NCOL + c] = (sA[adr] + sB[adr]) + sX[adr];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename F, bool HELM, bool TRI, int MINB>
+cudaError_t launch_warp(const hx_axlocal_args& a, cudaStream_t s) {
+  if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)a.n_elements;
+  if (a.n_col == 3)
+    ax8w<F, 3, HELM, TRI, MINB><<<grid, 32, 0, s>>>(a);
+  else
+    ax8w<F, 1, HELM, TRI, MINB><<<grid, 32, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
@@ -631,7 +917,8 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 // Kernel choice per variant (measured on B200, tools/sweep.py, profiles/):
 //  * trilinear family (FP64-bound): one CTA per element (ax8s), shared
-//    per-element setup, 8 CTAs/SM;
+//    per-element setup incl. the K00(j,k)/K11(i,k) tables, 10 CTAs/SM
+//    (96 registers, no spills);
 //  * stored / parallelepiped (HBM-bound): also one CTA per element — with
 //    8 CTAs/SM the plain coalesced loads reach 7.0 TB/s, ahead of the
 //    persistent TMA-prefetch pipeline (ax8, hook 1: 6.6 TB/s).
@@ -647,23 +934,33 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
     case HX_TRILINEAR:
       if (helm) {
         if (hook == 1) return launch<TrilinearPoly<true, false, false>, true, true>(*a, s);
+        if (hook == 2) return launch_single<TrilinearPoly<true, false, false, true, false, false, true>, true, true, 10>(*a, s);
         return launch_single<TrilinearPoly<true, false, false>, true, true, 8>(*a, s);
       }
       switch (hook) {
         case 1: return launch<TrilinearPoly<false, false, false>, false, true>(*a, s);
+        case 2: return launch_single<TrilinearPoly<false, false, false, true>, false, true, 8>(*a, s);
         case 6: return launch<TrilinearPoly<false, false, false>, false, true, 6>(*a, s);
         case 9: return launch<TrilinearPoly<false, false, false, false>, false, true, 6>(*a, s);
         case 10: return launch_single<TrilinearPoly<false, false, false, true>, false, true, 6>(*a, s);
         case 11: return launch_single<TrilinearPoly<false, false, false, false>, false, true, 6>(*a, s);
         case 13: return launch_single<TrilinearPoly<false, false, false, false>, false, true, 8>(*a, s);
-        default: return launch_single<TrilinearPoly<false, false, false, true>, false, true, 8>(*a, s);
+        case 14: return launch_single<TrilinearPoly<false, false, false, true, true>, false, true, 8>(*a, s);
+        case 16: return launch_single<TrilinearPoly<false, false, false, true, false, true>, false, true, 8>(*a, s);
+        case 19: return launch_single<TrilinearPoly<false, false, false, true, false, false>, false, true, 10>(*a, s);
+        case 20: return launch_warp<TrilinearPoly<false, false, false, true>, false, true, 15>(*a, s);
+        case 25: return launch_single<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 8>(*a, s);
+        case 27: return launch_double<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 8>(*a, s);
+        default: return launch_single<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 10>(*a, s);
       }
     case HX_TRILINEAR_PARTIAL:
       if (hook == 1) return launch<TrilinearPoly<false, false, true>, false, true>(*a, s);
-      return launch_single<TrilinearPoly<false, false, true>, false, true, 8>(*a, s);
+      if (hook == 2) return launch_single<TrilinearPoly<false, false, true>, false, true, 8>(*a, s);
+      return launch_single<TrilinearPoly<false, false, true, true, false, false, true>, false, true, 10>(*a, s);
     case HX_TRILINEAR_MERGED:
       if (hook == 1) return launch<TrilinearPoly<true, true, false>, true, true>(*a, s);
-      return launch_single<TrilinearPoly<true, true, false>, true, true, 8>(*a, s);
+      if (hook == 2) return launch_single<TrilinearPoly<true, true, false>, true, true, 8>(*a, s);
+      return launch_single<TrilinearPoly<true, true, false, true, false, false, true>, true, true, 10>(*a, s);
     case HX_STORED:
       if (hook == 1)
         return helm ? launch<StoredLoad<true>, true, false>(*a, s) : launch<StoredLoad<false>, false, false>(*a, s);
@@ -681,14 +978,15 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
 extern "C" cudaError_t hx_upload_basis_fast(int n1, const double* pts, const double* w, const double* d) {
   cudaError_t err = hx_upload_basis_local(n1, pts, w, d);
   if (err != cudaSuccess || n1 != 8) return err;
-  double eo[2][2][4][4];
-  for (int T = 0; T < 2; ++T)
-    for (int i = 0; i < 4; ++i)
-      for (int m = 0; m < 4; ++m) {
-        const double x = T ? d[m * 8 + i] : d[i * 8 + m];            // M[i][m]
-        const double y = T ? d[(7 - m) * 8 + i] : d[i * 8 + 7 - m];  // M[i][7-m]
-        eo[T][0][i][m] = 0.5 * (x + y);
-        eo[T][1][i][m] = 0.5 * (x - y);
-      }
+  double eo[2][2][2][4][4];
+  for (int cp = 0; cp < 2; ++cp)
+    for (int T = 0; T < 2; ++T)
+      for (int i = 0; i < 4; ++i)
+        for (int m = 0; m < 4; ++m) {
+          const double x = T ? d[m * 8 + i] : d[i * 8 + m];            // M[i][m]
+          const double y = T ? d[(7 - m) * 8 + i] : d[i * 8 + 7 - m];  // M[i][7-m]
+          eo[cp][T][0][i][m] = 0.5 * (x + y);
+          eo[cp][T][1][i][m] = 0.5 * (x - y);
+        }
   return cudaMemcpyToSymbol(c_EO, eo, sizeof(eo));
 }
