@@ -286,6 +286,33 @@ struct TrilinearPoly {
     }
   }
 
+  // adj(K(t_K)) entries (unscaled g of geometry.py:329-339).
+  template <int K>
+  __device__ __forceinline__ void adj_at(double g[6]) const {
+    const double t = cX<N1>(K);
+    const double a00 = TAB ? tab00[K] : fma(fma(k00[2], t, k00[1]), t, k00[0]);
+    const double a11 = TAB ? tab11[K] : fma(fma(k11[2], t, k11[1]), t, k11[0]);
+    const double a01 = fma(fma(k01[2], t, k01[1]), t, k01[0]);
+    const double a02 = fma(k02[1], t, k02[0]);
+    const double a12 = fma(k12[1], t, k12[0]);
+    g[0] = fma(a11, k22, -a12 * a12);
+    g[1] = fma(a02, a12, -a01 * k22);
+    g[2] = fma(a01, a12, -a02 * a11);
+    g[3] = fma(a00, k22, -a02 * a02);
+    g[4] = fma(a01, a02, -a00 * a12);
+    g[5] = fma(a00, a11, -a01 * a01);
+  }
+
+  // Factors of one node for multi-column application (see apply_factors):
+  // rr = g . (sin x) [* sout], the same operation order as node().
+  static constexpr bool kIn = true, kOut = false;
+  template <int K>
+  __device__ __forceinline__ void factors(int n, double g[6], double& sin, double& sout, double& mass) const {
+    adj_at<K>(g);
+    scale_at<K>(n, sin, mass);
+    sout = 1.0;
+  }
+
   // rr, ss, tt = scale * adj(K(t_K)) (x0, x1, x2).
   template <int K>
   __device__ __forceinline__ void apply_at(double scale, double x0, double x1, double x2, double& rr, double& ss,
@@ -337,6 +364,18 @@ struct StoredLoad {
     l0v = a.lam0_value;
     l1v = a.lam1_value;
   }
+  static constexpr bool kIn = false, kOut = HELM;  // rr = (g . x) * lam0 (axlocal.py:221-227 order)
+  template <int K>
+  __device__ __forceinline__ void factors(int n, double gg[6], double& sin, double& sout, double& mass) const {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) gg[q] = __ldg(g + q * N3 + n);
+    sin = sout = 1.0;
+    mass = 0.0;
+    if (HELM) {
+      sout = lam0 ? __ldg(lam0 + n) : l0v;
+      mass = (lam1 ? __ldg(lam1 + n) : l1v) * __ldg(gwj + n);
+    }
+  }
   template <int K>
   __device__ __forceinline__ void node(int n, double x0, double x1, double x2, double& rr, double& ss, double& tt,
                                        double& mass) const {
@@ -377,6 +416,20 @@ struct Ppd {
     lam1 = a.lam1 ? a.lam1 + e * N3 : nullptr;
     l0v = a.lam0_value;
     l1v = a.lam1_value;
+  }
+  static constexpr bool kIn = true, kOut = HELM;  // x scaled by w before h (node order), then lam0
+  template <int K>
+  __device__ __forceinline__ void factors(int n, double gg[6], double& sin, double& sout, double& mass) const {
+    const double w = (cW<N1>(K) * wj) * wi;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) gg[q] = h[q];
+    sin = w;
+    sout = 1.0;
+    mass = 0.0;
+    if (HELM) {
+      sout = lam0 ? __ldg(lam0 + n) : l0v;
+      mass = (lam1 ? __ldg(lam1 + n) : l1v) * (w * h[6]);
+    }
   }
   template <int K>
   __device__ __forceinline__ void node(int n, double x0, double x1, double x2, double& rr, double& ss, double& tt,
@@ -723,6 +776,146 @@ cudaError_t launch_double(const hx_axlocal_args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// n_col = 3 with factor reuse (the paper's loop swap, §4.1): all three columns
+// go through every phase together, each node's factors are computed once and
+// applied to the three columns with exactly the per-column arithmetic of the
+// n_col = 1 kernel (so n_col=3 == 3 x n_col=1 bitwise, test_axlocal.py:206-225).
+static __shared__ double s_c3X[3][CUBE];
+static __shared__ double s_c3A[3][CUBE];
+static __shared__ double s_c3B[3][CUBE];
+
+template <typename F>
+__device__ __forceinline__ void apply_factors(const double g[6], double sin, double sout, double x0, double x1,
+                                              double x2, double& rr, double& ss, double& tt) {
+  double s0 = x0, s1 = x1, s2 = x2;
+  if (F::kIn) {
+    s0 = sin * x0;
+    s1 = sin * x1;
+    s2 = sin * x2;
+  }
+  rr = fma(g[0], s0, fma(g[1], s1, g[2] * s2));
+  ss = fma(g[1], s0, fma(g[3], s1, g[4] * s2));
+  tt = fma(g[2], s0, fma(g[4], s1, g[5] * s2));
+  if (F::kOut) {
+    rr *= sout;
+    ss *= sout;
+    tt *= sout;
+  }
+}
+
+template <typename F, bool HELM, bool TRI, int MINB>
+__global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axlocal_args a) {
+  constexpr int NC = 3;
+  const int64_t e = blockIdx.x;
+  const int t = threadIdx.x;
+  const Roles r = roles(t);
+  const int kp = Aj(r.fj) + r.fi;
+  const int rb = Ak(r.rk) + Aj(r.rj);
+  const int cb = Ak(r.ck) + r.ci;
+  const int lin = r.fj * 8 + r.fi;
+  if (TRI && t < 24) s_verts[0][t] = __ldg(a.verts + e * 24 + t);
+  if (TRI) __syncthreads();
+
+  // P0: the three columns of the k-fibre; x2 = D_t x in registers
+  double x2[NC][8];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double xk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xk[k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_c3X[c][Ak(k) + kp] = xk[k];
+    eo8<0>(xk, x2[c]);
+  }
+  if (TRI && F::kStageA) tri_stage_a(t, s_verts[0], s_tri);
+  __syncthreads();
+
+  // P1: forward r (i-rows) and s (j-columns) derivatives of the three columns
+  F fac;
+  fac.prepare(a, e, s_tri, s_verts[0], r.fi, r.fj);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double v[8], o[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) v[n] = s_c3X[c][rb + n];
+    eo8<0>(v, o);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s_c3A[c][rb + n] = o[n];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) v[n] = s_c3X[c][cb + Aj(n)];
+    eo8<0>(v, o);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s_c3B[c][cb + Aj(n)] = o[n];
+  }
+  __syncthreads();
+
+  // P2: factors once per node, applied to the three columns; tt parked in the
+  // (consumed) x cube at this thread's own fibre positions
+  double mass[8];
+#define HX_NODE3(K)                                                                       \
+  {                                                                                       \
+    const int adr = Ak(K) + kp;                                                           \
+    double g[6], sin, sout;                                                               \
+    fac.template factors<K>(K * 64 + lin, g, sin, sout, mass[K]);                         \
+    _Pragma("unroll") for (int c = 0; c < NC; ++c) {                                      \
+      double rr, ss, tt;                                                                  \
+      apply_factors<F>(g, sin, sout, s_c3A[c][adr], s_c3B[c][adr], x2[c][K], rr, ss, tt); \
+      s_c3A[c][adr] = rr;                                                                 \
+      s_c3B[c][adr] = ss;                                                                 \
+      s_c3X[c][adr] = tt;                                                                 \
+    }                                                                                     \
+  }
+  HX_NODE3(0) HX_NODE3(1) HX_NODE3(2) HX_NODE3(3) HX_NODE3(4) HX_NODE3(5) HX_NODE3(6) HX_NODE3(7)
+#undef HX_NODE3
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double tt[8], yt[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tt[k] = s_c3X[c][Ak(k) + kp];
+    eo8<1>(tt, yt);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_c3X[c][Ak(k) + kp] = yt[k];
+  }
+  __syncthreads();
+
+  // P3: transposed r and s contractions, in place
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double v[8], o[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) v[n] = s_c3A[c][rb + n];
+    eo8<1>(v, o);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s_c3A[c][rb + n] = o[n];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) v[n] = s_c3B[c][cb + Aj(n)];
+    eo8<1>(v, o);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s_c3B[c][cb + Aj(n)] = o[n];
+  }
+  __syncthreads();
+
+  // P4: y = D_r^T rr + D_s^T ss + D_t^T tt [+ mass x] (n_col = 1 order)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int adr = Ak(k) + kp;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double y = (s_c3A[c][adr] + s_c3B[c][adr]) + s_c3X[c][adr];
+      if (HELM) y += mass[k] * __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
+      a.y[(e * N3 + k * 64 + lin) * NC + c] = y;
+    }
+  }
+}
+
+template <typename F, bool HELM, bool TRI, int MINB = 5>
+cudaError_t launch_c3(const hx_axlocal_args& a, cudaStream_t s) {
+  if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
+  ax8c3<F, HELM, TRI, MINB><<<(unsigned)a.n_elements, 64, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
 __global__ void __launch_bounds__(64, MINB) ax8(const __grid_constant__ hx_axlocal_args a) {
   const int t = threadIdx.x;
@@ -930,6 +1123,22 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
   if (!aligned16(a->x) || (a->verts && !aligned16(a->verts))) return cudaErrorNotSupported;
   const bool helm = a->equation == HX_HELMHOLTZ;
   const int hook = a->reserved;
+  if (a->n_col == 3 && hook != 4) {
+    switch (a->factor_source) {
+      case HX_TRILINEAR:
+        return helm ? launch_c3<TrilinearPoly<true, false, false, true, false, false, true>, true, true>(*a, s)
+                    : launch_c3<TrilinearPoly<false, false, false, true, false, false, true>, false, true>(*a, s);
+      case HX_TRILINEAR_PARTIAL:
+        return launch_c3<TrilinearPoly<false, false, true, true, false, false, true>, false, true>(*a, s);
+      case HX_TRILINEAR_MERGED:
+        return launch_c3<TrilinearPoly<true, true, false, true, false, false, true>, true, true>(*a, s);
+      case HX_STORED:
+        return helm ? launch_c3<StoredLoad<true>, true, false>(*a, s) : launch_c3<StoredLoad<false>, false, false>(*a, s);
+      case HX_PARALLELEPIPED:
+        return helm ? launch_c3<Ppd<true>, true, false>(*a, s) : launch_c3<Ppd<false>, false, false>(*a, s);
+    }
+    return cudaErrorNotSupported;
+  }
   switch (a->factor_source) {
     case HX_TRILINEAR:
       if (helm) {

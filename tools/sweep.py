@@ -56,8 +56,13 @@ def main():
         ("helmholtz", 1, "stored", 0, 0),
         ("helmholtz", 1, "parallelepiped", 0, 0),
         ("poisson", 3, "trilinear", 0, 0),
+        ("poisson", 3, "trilinear", 0, 4),
         ("poisson", 3, "stored", 0, 0),
+        ("poisson", 3, "stored", 0, 4),
+        ("poisson", 3, "parallelepiped", 0, 0),
         ("helmholtz", 3, "trilinear", 0, 0),
+        ("helmholtz", 3, "trilinear", 0, 4),
+        ("helmholtz", 3, "trilinear-merged", 0, 0),
     ]
     prepared = []
     for eq, ncol, src, kernel, hook in cases:
