@@ -9,7 +9,7 @@ OBJ       := build/obj
 LIB       := paper_2504_07042_b200/_lib/libhx_axlocal.so
 ORDERS    := 2 3 4 5 6 7 8 9 10 11 12 13 14 15 16
 GEN_OBJS  := $(foreach n,$(ORDERS),$(OBJ)/ax_generic_$(n).o)
-OBJS      := $(GEN_OBJS) $(OBJ)/ax_fast.o $(OBJ)/setup.o $(OBJ)/capi.o
+OBJS      := $(GEN_OBJS) $(OBJ)/ax_fast.o $(OBJ)/setup.o $(OBJ)/bp5.o $(OBJ)/capi.o
 HEADERS   := $(SRC)/hx_common.cuh include/hx_axlocal.h $(wildcard $(SRC)/*.cuh)
 
 all: $(LIB)

@@ -152,6 +152,45 @@ int hx_setup_parallelepiped(int64_t n_elements, const double* verts, double* h_o
  */
 int hx_classify_elements(int64_t n_elements, const double* verts, int8_t* kind_out, void* stream);
 
+/* ------------------------------------------------------------------------
+ * BP5 / Nekbone CG proxy on a structured box (reference solver.py:64-308).
+ * A rank owns element z-layers [z0, z0+nz_el) of an ex x ey x ez box of
+ * order N; its global vectors are the slab lattice
+ * (ex*N+1) x (ey*N+1) x (nz_el*N+1), x fastest (mesh.py:271-274 numbering
+ * restricted to the slab, both interface planes included).
+ */
+typedef struct {
+  int32_t order;  /* N */
+  int32_t ex, ey; /* elements along x and y */
+  int32_t nz_el;  /* element layers in this slab */
+  int32_t z0;     /* first global element layer of the slab */
+  int32_t ez;     /* global element layers (physical boundary at 0 and ez*N) */
+  int32_t n_col;  /* columns of the element-local array (1 or 3) */
+  int32_t col;    /* which column gather writes / scatter-add reads */
+} hx_box;
+
+/* xl[:, :, col] (E_slab, n1^3, n_col) = Q u: copy lattice values to element-local
+ * storage (gather, mesh.py:286-294); the lattice index is computed, not loaded. */
+int hx_bp5_gather(const hx_box* box, const double* u, double* xl, void* stream);
+
+/* v = Q^T yl[:, :, col] on the slab lattice (scatter_add, mesh.py:297-313): owner-computes,
+ * each node sums its element copies in ascending element index, the
+ * np.bincount order; interface planes hold this slab's partial sums. */
+int hx_bp5_scatter_add(const hx_box* box, const double* yl, double* v, void* stream);
+
+/* v = 0 on the physical boundary of the box (boundary_node_mask, mesh.py:316-335). */
+int hx_bp5_mask(const hx_box* box, double* v, void* stream);
+
+/* *out = sum_{lo <= i < hi} a[i] b[i] on the device, fixed reduction tree
+ * (bitwise reproducible); work holds >= 1184 doubles. */
+int hx_dot(const double* a, const double* b, int64_t lo, int64_t hi, double* work, double* out, void* stream);
+
+/* CG updates (solver.py:158-170) with device scalars scal = {rr, pap, rr_new}:
+ * x += (rr/pap) p, r -= (rr/pap) ap  — and —  p = r + (rr_new/rr) p. */
+int hx_cg_update_xr(const double* scal, double* x, const double* p, double* r, const double* ap, int64_t n,
+                    void* stream);
+int hx_cg_update_p(const double* scal, double* p, const double* r, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

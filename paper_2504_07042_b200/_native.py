@@ -13,7 +13,7 @@ import ctypes
 import os
 import threading
 
-__all__ = ["lib", "AxArgs", "check", "LIB_PATH", "SYMBOLS"]
+__all__ = ["lib", "AxArgs", "Box", "check", "LIB_PATH", "SYMBOLS"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libhx_axlocal.so")
 
@@ -29,6 +29,12 @@ SYMBOLS = (
     "hx_setup_stored",
     "hx_setup_parallelepiped",
     "hx_classify_elements",
+    "hx_bp5_gather",
+    "hx_bp5_scatter_add",
+    "hx_bp5_mask",
+    "hx_dot",
+    "hx_cg_update_xr",
+    "hx_cg_update_p",
 )
 
 HX_OK, HX_ERR_INVALID, HX_ERR_GEOMETRY, HX_ERR_CUDA, HX_ERR_UNSUPPORTED = range(5)
@@ -64,6 +70,13 @@ class AxArgs(ctypes.Structure):
     ]
 
 
+class Box(ctypes.Structure):
+    """Mirror of ``hx_box`` (include/hx_axlocal.h)."""
+
+    _fields_ = [("order", _i32), ("ex", _i32), ("ey", _i32), ("nz_el", _i32), ("z0", _i32), ("ez", _i32),
+                ("n_col", _i32), ("col", _i32)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -95,6 +108,18 @@ def _load():
     so.hx_setup_parallelepiped.argtypes = [_i64, _c_p, _c_p, _c_p, _c_p]
     so.hx_classify_elements.restype = ctypes.c_int
     so.hx_classify_elements.argtypes = [_i64, _c_p, _c_p, _c_p]
+    bp = ctypes.POINTER(Box)
+    for name, args in (
+        ("hx_bp5_gather", [bp, _c_p, _c_p, _c_p]),
+        ("hx_bp5_scatter_add", [bp, _c_p, _c_p, _c_p]),
+        ("hx_bp5_mask", [bp, _c_p, _c_p]),
+        ("hx_dot", [_c_p, _c_p, _i64, _i64, _c_p, _c_p, _c_p]),
+        ("hx_cg_update_xr", [_c_p, _c_p, _c_p, _c_p, _c_p, _i64, _c_p]),
+        ("hx_cg_update_p", [_c_p, _c_p, _c_p, _i64, _c_p]),
+    ):
+        fn = getattr(so, name)
+        fn.restype = ctypes.c_int
+        fn.argtypes = args
     return so
 
 

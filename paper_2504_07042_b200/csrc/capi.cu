@@ -42,6 +42,12 @@ cudaError_t hx_setup_trilinear_impl(int, int64_t, const double*, int, int64_t*, 
 cudaError_t hx_setup_stored_impl(int, int64_t, const double*, double*, double*, int64_t*, cudaStream_t);
 cudaError_t hx_setup_ppd_impl(int64_t, const double*, double*, int64_t*, cudaStream_t);
 cudaError_t hx_classify_impl(int64_t, const double*, int8_t*, cudaStream_t);
+cudaError_t hx_bp5_gather_impl(hx_box, const double*, double*, cudaStream_t);
+cudaError_t hx_bp5_scatter_impl(hx_box, const double*, double*, cudaStream_t);
+cudaError_t hx_bp5_mask_impl(hx_box, double*, cudaStream_t);
+cudaError_t hx_dot_impl(const double*, const double*, int64_t, int64_t, double*, double*, cudaStream_t);
+cudaError_t hx_cg_xr_impl(const double*, double*, const double*, double*, const double*, int64_t, cudaStream_t);
+cudaError_t hx_cg_p_impl(const double*, double*, const double*, int64_t, cudaStream_t);
 }
 
 namespace {
@@ -208,4 +214,58 @@ extern "C" int hx_classify_elements(int64_t E, const double* verts, int8_t* kind
   g_last_error.clear();
   if (!verts || !kind) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_classify_impl(E, verts, kind, static_cast<cudaStream_t>(stream)), "hx_classify_elements");
+}
+
+namespace {
+int box_ok(const hx_box* b) {
+  if (!b) return fail(HX_ERR_INVALID, "null box");
+  if (!order_ok(b->order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
+  if (b->ex < 1 || b->ey < 1 || b->nz_el < 1 || b->ez < 1 || b->z0 < 0 || b->z0 + b->nz_el > b->ez)
+    return fail(HX_ERR_INVALID, "bad box / slab extents");
+  if ((b->n_col != 1 && b->n_col != 3) || b->col < 0 || b->col >= b->n_col)
+    return fail(HX_ERR_INVALID, "bad column selection");
+  return HX_OK;
+}
+}  // namespace
+
+extern "C" int hx_bp5_gather(const hx_box* box, const double* u, double* xl, void* stream) {
+  g_last_error.clear();
+  if (int st = box_ok(box)) return st;
+  if (!u || !xl) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_bp5_gather_impl(*box, u, xl, static_cast<cudaStream_t>(stream)), "hx_bp5_gather");
+}
+
+extern "C" int hx_bp5_scatter_add(const hx_box* box, const double* yl, double* v, void* stream) {
+  g_last_error.clear();
+  if (int st = box_ok(box)) return st;
+  if (!yl || !v) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_bp5_scatter_impl(*box, yl, v, static_cast<cudaStream_t>(stream)), "hx_bp5_scatter_add");
+}
+
+extern "C" int hx_bp5_mask(const hx_box* box, double* v, void* stream) {
+  g_last_error.clear();
+  if (int st = box_ok(box)) return st;
+  if (!v) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_bp5_mask_impl(*box, v, static_cast<cudaStream_t>(stream)), "hx_bp5_mask");
+}
+
+extern "C" int hx_dot(const double* a, const double* b, int64_t lo, int64_t hi, double* work, double* out,
+                      void* stream) {
+  g_last_error.clear();
+  if (!a || !b || !work || !out) return fail(HX_ERR_INVALID, "null pointer");
+  if (lo < 0 || hi < lo) return fail(HX_ERR_INVALID, "bad range");
+  return cuda_status(hx_dot_impl(a, b, lo, hi, work, out, static_cast<cudaStream_t>(stream)), "hx_dot");
+}
+
+extern "C" int hx_cg_update_xr(const double* scal, double* x, const double* p, double* r, const double* ap,
+                               int64_t n, void* stream) {
+  g_last_error.clear();
+  if (!scal || !x || !p || !r || !ap || n < 0) return fail(HX_ERR_INVALID, "bad arguments");
+  return cuda_status(hx_cg_xr_impl(scal, x, p, r, ap, n, static_cast<cudaStream_t>(stream)), "hx_cg_update_xr");
+}
+
+extern "C" int hx_cg_update_p(const double* scal, double* p, const double* r, int64_t n, void* stream) {
+  g_last_error.clear();
+  if (!scal || !p || !r || n < 0) return fail(HX_ERR_INVALID, "bad arguments");
+  return cuda_status(hx_cg_p_impl(scal, p, r, n, static_cast<cudaStream_t>(stream)), "hx_cg_update_p");
 }

@@ -119,6 +119,22 @@ def main():
             arrays[f"dense_{eq}_{order}_verts"] = el.vertices
             arrays[f"dense_{eq}_{order}"] = dense_local_matrix(spec, el, SpectralBasis.build(order))
 
+    # Nekbone CG protocol (solver.py:240-308): iterations and max-norm error per variant
+    from hosfem.solver import NekboneConfig, nekbone_benchmark
+
+    nek = []
+    for cfg in (
+        dict(order=5, elements=(3, 3, 3), equation="poisson", n_col=1, perturbation=0.0),
+        dict(order=3, elements=(4, 3, 2), equation="poisson", n_col=1, perturbation=0.15),
+        dict(order=4, elements=(2, 2, 3), equation="helmholtz", n_col=1, perturbation=0.1),
+        dict(order=3, elements=(2, 2, 2), equation="poisson", n_col=3, perturbation=0.1),
+    ):
+        res, _ = nekbone_benchmark(NekboneConfig(order=cfg["order"], elements=cfg["elements"],
+                                                 equation=Equation(cfg["equation"]), n_col=cfg["n_col"],
+                                                 perturbation=cfg["perturbation"], tol=1e-8, max_iter=300))
+        nek.append(dict(cfg, results=[dict(variant=r.variant, iterations=r.iterations, error=r.error) for r in res]))
+    arrays["nekbone_json"] = np.frombuffer(json.dumps(nek).encode(), dtype=np.uint8)
+
     arrays["cases_json"] = np.frombuffer(json.dumps(cases).encode(), dtype=np.uint8)
     np.savez_compressed(OUT, **arrays)
     print(f"wrote {OUT}: {len(cases)} operator cases, {os.path.getsize(OUT) / 1e6:.2f} MB")

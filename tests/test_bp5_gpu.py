@@ -1,0 +1,92 @@
+"""BP5 / Nekbone on the GPU (needs a B200): gather / scatter-add / mask
+kernels against the reference's definitions, the global operator, and the CG
+proxy against the reference's own Nekbone results (golden)."""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2504_07042_b200 as hx
+from oracle import hosfem_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2504_07042_b200 import solver as S  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.mark.parametrize("order,counts,n_col", [(1, (3, 2, 2), 1), (3, (4, 3, 2), 1), (7, (2, 3, 4), 3), (5, (1, 1, 1), 1)])
+def test_gather_scatter_mask_bitwise(order, counts, n_col):
+    ex, ey, ez = counts
+    L = S.SlabLayout(counts, order)
+    l2g = O.box_l2g(ex, ey, ez, order)
+    rng = np.random.default_rng(order)
+    be = S.CudaBackend(DEV)
+    u = rng.standard_normal(L.n_local)
+    xl = torch.empty((L.n_elements, (order + 1) ** 3, n_col), dtype=torch.float64, device=DEV)
+    for c in range(n_col):
+        be.gather(L, torch.as_tensor(u, device=DEV), xl, n_col, c)
+        assert np.array_equal(xl[:, :, c].cpu().numpy(), O.gather(u, l2g)[:, :, 0])
+    yl = rng.standard_normal((L.n_elements, (order + 1) ** 3, n_col))
+    for c in range(n_col):
+        v = torch.empty(L.n_local, dtype=torch.float64, device=DEV)
+        be.scatter(L, torch.as_tensor(yl, device=DEV), v, n_col, c)
+        # owner-computes in ascending element order == np.bincount, bit for bit
+        assert np.array_equal(v.cpu().numpy(), O.scatter_add(yl[:, :, c], l2g, L.n_local))
+    v = torch.ones(L.n_local, dtype=torch.float64, device=DEV)
+    be.mask(L, v)
+    assert np.array_equal(v.cpu().numpy().astype(bool), O.interior_mask(ex, ey, ez, order))
+
+
+def test_dot_is_deterministic_and_accurate():
+    be = S.CudaBackend(DEV)
+    a = torch.randn(3_000_001, dtype=torch.float64, device=DEV)
+    b = torch.randn(3_000_001, dtype=torch.float64, device=DEV)
+    out1 = torch.zeros(1, dtype=torch.float64, device=DEV)
+    out2 = torch.zeros(1, dtype=torch.float64, device=DEV)
+    be.dot(a, b, a.numel(), out1)
+    be.dot(a, b, a.numel(), out2)
+    assert torch.equal(out1, out2)
+    want = float(np.dot(a.cpu().numpy(), b.cpu().numpy()))
+    assert abs(out1.item() - want) <= 1e-12 * np.sqrt(a.numel())
+
+
+@pytest.mark.parametrize("src,eq", [("trilinear", "poisson"), ("stored", "poisson"), ("trilinear-merged", "helmholtz")])
+def test_global_operator_matches_oracle(src, eq):
+    order, counts = 5, (3, 2, 2)
+    mesh = hx.box_mesh(*counts, order, perturbation=0.15, seed=3)
+    kw = {"lam0": 1.3, "lam1": 0.4} if eq == "helmholtz" else {}
+    op = S.GlobalOperator(mesh, hx.KernelSpec(eq, 1, src, order), hx.SpectralBasis.build(order), **kw)
+    u = np.random.default_rng(1).standard_normal(op.layout.n_local)
+    got = op.apply_global(u)
+    l2g = O.box_l2g(*counts, order)
+    st = O.setup(src, eq, order, mesh.vertices, kw.get("lam0"), kw.get("lam1"))
+    want = O.scatter_add(O.apply_setup(st, O.gather(u, l2g)), l2g, op.layout.n_local)
+    assert O.rel_diff(got, want) <= 1e-12
+
+
+def test_nekbone_matches_reference_golden(golden):
+    """Table-5 parity observable: same CG iteration count, same error level."""
+    for cfg in json.loads(bytes(golden["nekbone_json"]).decode()):
+        conf = S.NekboneConfig(order=cfg["order"], elements=tuple(cfg["elements"]), equation=cfg["equation"],
+                               n_col=cfg["n_col"], perturbation=cfg["perturbation"], tol=1e-8, max_iter=300)
+        res, _ = S.nekbone_benchmark(conf)
+        for r, want in zip(res, cfg["results"]):
+            assert r.variant == want["variant"]
+            assert abs(r.iterations - want["iterations"]) <= 1, (cfg, r)
+            assert r.error == pytest.approx(want["error"], rel=5e-2), (cfg, r)
+
+
+def test_cg_is_bitwise_reproducible():
+    mesh = hx.box_mesh(4, 4, 4, 7, perturbation=0.1, seed=0)
+    op = S.GlobalOperator(mesh, hx.KernelSpec("poisson", 1, "trilinear", 7), hx.SpectralBasis.build(7))
+    b = torch.randn(op.layout.n_local, dtype=torch.float64, device=DEV)
+    r1 = S.cg_solve(op, b, tol=1e-8, max_iter=50)
+    r2 = S.cg_solve(op, b, tol=1e-8, max_iter=50)
+    assert r1.iterations == r2.iterations and r1.residual_history == r2.residual_history
+    assert torch.equal(r1.solution, r2.solution)

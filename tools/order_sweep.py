@@ -1,0 +1,80 @@
+"""C3 (BASELINE configs[2]): polynomial-order sweep N=1..15 at ~100 M DOF on one GPU.
+
+    python tools/order_sweep.py [--dof 1e8] [--variants trilinear,parallelepiped,stored]
+
+Mesh per order: e^3 elements with e = round((dof / n1^3)^(1/3)), trilinear =
+box_mesh(e,e,e,N, pert 0.1, seed 0), parallelepiped = the unperturbed box under a global
+shear.  Prints GDOF/s and the fraction of the per-variant roofline (reference work model,
+D on chip; FP64 37.0 TF measured, HBM 6550 GB/s).
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2504_07042_b200 as hx  # noqa: E402
+from paper_2504_07042_b200.workload import workload_count  # noqa: E402
+
+FP64, HBM = 37.0e12, 6.5501e12
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dof", type=float, default=1e8)
+    ap.add_argument("--orders", default="1,2,3,4,5,6,7,8,9,10,11,12,13,14,15")
+    ap.add_argument("--variants", default="trilinear,parallelepiped,stored")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    shear = torch.tensor([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]], dtype=torch.float64, device=dev)
+    rows = []
+    for order in (int(v) for v in args.orders.split(",")):
+        n1 = order + 1
+        e = max(1, round((args.dof / n1**3) ** (1.0 / 3.0)))
+        basis = hx.SpectralBasis.build(order)
+        for var in args.variants.split(","):
+            if var == "parallelepiped":
+                verts = hx.box_mesh(e, e, e, order).vertices_device(dev) @ shear.T
+            else:
+                verts = hx.box_mesh(e, e, e, order, perturbation=0.1, seed=0).vertices_device(dev)
+            spec = hx.KernelSpec("poisson", 1, var, order)
+            op = hx.LocalOperator(spec, verts, basis, device=dev)
+            E = verts.shape[0]
+            x = torch.randn((E, n1**3, 1), dtype=torch.float64, device=dev)
+            y = torch.empty_like(x)
+            for _ in range(2):
+                op.apply_(x, y)
+            torch.cuda.synchronize()
+            time.sleep(0.2)
+            s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(args.reps):
+                op.apply_(x, y)
+            t.record()
+            t.synchronize()
+            ms = s.elapsed_time(t) / args.reps
+            wc = workload_count(spec, include_dmat_traffic=False)
+            t_model = max((wc.f_ax + wc.f_geo) / FP64, wc.m_bytes / HBM) * E
+            frac = t_model / (ms * 1e-3)
+            gdofs = E * n1**3 / (ms * 1e-3) / 1e9
+            kernel = "specialised" if order == 7 else "generic"
+            row = dict(order=order, variant=var, elements=E, dof=E * n1**3, ms=ms, gdofs=gdofs, roofline_frac=frac,
+                       kernel=kernel)
+            rows.append(row)
+            print(f"N={order:2d} {var:15s} E={E:9d} ({E * n1**3 / 1e6:6.1f} M DOF) {ms:8.3f} ms "
+                  f"{gdofs:7.1f} GDOF/s  {100 * frac:5.1f}% of roofline  [{kernel}]", flush=True)
+            del op, x, y, verts
+            torch.cuda.empty_cache()
+    if args.json:
+        with open(args.json, "w") as fh:
+            json.dump(rows, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
