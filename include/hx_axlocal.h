@@ -49,6 +49,23 @@ typedef enum {
   HX_PARALLELEPIPED = 4
 } hx_factor_source;
 
+/* ------------------------------------------------------------------------
+ * BP5 / Nekbone CG proxy on a structured box (reference solver.py:64-308).
+ * A rank owns element z-layers [z0, z0+nz_el) of an ex x ey x ez box of
+ * order N; its global vectors are the slab lattice
+ * (ex*N+1) x (ey*N+1) x (nz_el*N+1), x fastest (mesh.py:271-274 numbering
+ * restricted to the slab, both interface planes included).
+ */
+typedef struct {
+  int32_t order;  /* N */
+  int32_t ex, ey; /* elements along x and y */
+  int32_t nz_el;  /* element layers in this slab */
+  int32_t z0;     /* first global element layer of the slab */
+  int32_t ez;     /* global element layers (physical boundary at 0 and ez*N) */
+  int32_t n_col;  /* columns of the element-local array (1 or 3) */
+  int32_t col;    /* which column gather writes / scatter-add reads */
+} hx_box;
+
 /*
  * Arguments of one apply.  Replaces LocalOperator.apply/_apply_range/_factor_stage
  * (axlocal.py:171-258): y = A x for all E elements of the operator.
@@ -83,6 +100,13 @@ typedef struct {
   double lam1_value;
   int32_t kernel;         /* 0 = best available; 1 = generic slice kernel (test hook) */
   int32_t reserved;
+  /* Optional fused gather (BP5): when gather != 0, x is NOT element-local but
+   * the slab lattice vector of gather_box and each element reads its nodes
+   * straight from it (Q u, mesh.py:286-294).  Order 7, n_col 1, and the
+   * elements must be the box's slab in its element order. */
+  int32_t gather;
+  int32_t reserved2;
+  hx_box gather_box;
 } hx_axlocal_args;
 
 /* Library version string. */
@@ -152,22 +176,7 @@ int hx_setup_parallelepiped(int64_t n_elements, const double* verts, double* h_o
  */
 int hx_classify_elements(int64_t n_elements, const double* verts, int8_t* kind_out, void* stream);
 
-/* ------------------------------------------------------------------------
- * BP5 / Nekbone CG proxy on a structured box (reference solver.py:64-308).
- * A rank owns element z-layers [z0, z0+nz_el) of an ex x ey x ez box of
- * order N; its global vectors are the slab lattice
- * (ex*N+1) x (ey*N+1) x (nz_el*N+1), x fastest (mesh.py:271-274 numbering
- * restricted to the slab, both interface planes included).
- */
-typedef struct {
-  int32_t order;  /* N */
-  int32_t ex, ey; /* elements along x and y */
-  int32_t nz_el;  /* element layers in this slab */
-  int32_t z0;     /* first global element layer of the slab */
-  int32_t ez;     /* global element layers (physical boundary at 0 and ez*N) */
-  int32_t n_col;  /* columns of the element-local array (1 or 3) */
-  int32_t col;    /* which column gather writes / scatter-add reads */
-} hx_box;
+
 
 /* xl[:, :, col] (E_slab, n1^3, n_col) = Q u: copy lattice values to element-local
  * storage (gather, mesh.py:286-294); the lattice index is computed, not loaded. */
@@ -180,6 +189,16 @@ int hx_bp5_scatter_add(const hx_box* box, const double* yl, double* v, void* str
 
 /* v = 0 on the physical boundary of the box (boundary_node_mask, mesh.py:316-335). */
 int hx_bp5_mask(const hx_box* box, double* v, void* stream);
+
+/* Fused CG step pieces:
+ *  hx_bp5_scatter_dot: v = mask(Q^T yl) and *out = sum_{i < n_owned} p[i] v[i]
+ *    (the pap of solver.py:152-153; v = ap);
+ *  hx_cg_update_xr_dot: x += (rr/pap) p, r -= (rr/pap) ap and *out = sum_{i < n_owned} r[i]^2.
+ * Both reduce in a fixed tree (work >= 1184 doubles). */
+int hx_bp5_scatter_dot(const hx_box* box, const double* yl, double* v, const double* p, int64_t n_owned,
+                       double* work, double* out, void* stream);
+int hx_cg_update_xr_dot(const double* scal, double* x, const double* p, double* r, const double* ap, int64_t n,
+                        int64_t n_owned, double* work, double* out, void* stream);
 
 /* *out = sum_{lo <= i < hi} a[i] b[i] on the device, fixed reduction tree
  * (bitwise reproducible); work holds >= 1184 doubles. */

@@ -35,12 +35,21 @@ SYMBOLS = (
     "hx_dot",
     "hx_cg_update_xr",
     "hx_cg_update_p",
+    "hx_bp5_scatter_dot",
+    "hx_cg_update_xr_dot",
 )
 
 HX_OK, HX_ERR_INVALID, HX_ERR_GEOMETRY, HX_ERR_CUDA, HX_ERR_UNSUPPORTED = range(5)
 
 _c_p = ctypes.c_void_p
 _i32, _i64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+
+class Box(ctypes.Structure):
+    """Mirror of ``hx_box`` (include/hx_axlocal.h)."""
+
+    _fields_ = [("order", _i32), ("ex", _i32), ("ey", _i32), ("nz_el", _i32), ("z0", _i32), ("ez", _i32),
+                ("n_col", _i32), ("col", _i32)]
 
 
 class AxArgs(ctypes.Structure):
@@ -67,14 +76,10 @@ class AxArgs(ctypes.Structure):
         ("lam1_value", _f64),
         ("kernel", _i32),
         ("reserved", _i32),
+        ("gather", _i32),
+        ("reserved2", _i32),
+        ("gather_box", Box),
     ]
-
-
-class Box(ctypes.Structure):
-    """Mirror of ``hx_box`` (include/hx_axlocal.h)."""
-
-    _fields_ = [("order", _i32), ("ex", _i32), ("ey", _i32), ("nz_el", _i32), ("z0", _i32), ("ez", _i32),
-                ("n_col", _i32), ("col", _i32)]
 
 
 _lock = threading.Lock()
@@ -116,6 +121,8 @@ def _load():
         ("hx_dot", [_c_p, _c_p, _i64, _i64, _c_p, _c_p, _c_p]),
         ("hx_cg_update_xr", [_c_p, _c_p, _c_p, _c_p, _c_p, _i64, _c_p]),
         ("hx_cg_update_p", [_c_p, _c_p, _c_p, _i64, _c_p]),
+        ("hx_bp5_scatter_dot", [bp, _c_p, _c_p, _c_p, _i64, _c_p, _c_p, _c_p]),
+        ("hx_cg_update_xr_dot", [_c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _c_p, _c_p, _c_p]),
     ):
         fn = getattr(so, name)
         fn.restype = ctypes.c_int

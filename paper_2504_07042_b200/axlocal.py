@@ -317,6 +317,15 @@ class LocalOperator:
         s = _stream(self.device) if stream is None else ctypes.c_void_p(stream)
         _native.check(_native.lib().hx_axlocal(ctypes.byref(args), s))
 
+    def apply_lattice_(self, u, y, box, stream=None):
+        """y = A Q u: the element-local x gathered on the fly from the slab lattice
+        vector u of ``box`` (fused BP5 gather; order 7, one column)."""
+        args = self._args(u.data_ptr(), y.data_ptr())
+        args.gather = 1
+        args.gather_box = box
+        self._launch(args, stream)
+        return y
+
     def apply_(self, x, y, stream=None):
         """y = A x for contiguous fp64 device tensors (E, n1^3, n_col); stream-ordered,
         no allocation, no synchronisation."""

@@ -608,12 +608,22 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
   const int cb = Ak(r.ck) + r.ci;      // j-column base (+ Aj(n))
   const int lin = r.fj * 8 + r.fi;     // k-fibre offset in the linear element (+ 64 k)
 
+  // element-local x, or (fused BP5 gather) the slab lattice: node (i,j,k) of
+  // element (cx,cy,cz) is lattice point (cx N + i, cy N + j, cz N + k)
+  int64_t xoff = (e * N3 + lin) * NCOL, xstr = 64 * NCOL;
+  if (!XLAND && a.gather) {
+    const hx_box& bx = a.gather_box;
+    const int64_t nx = (int64_t)bx.ex * 7 + 1, ny = (int64_t)bx.ey * 7 + 1;
+    const int64_t cx = e % bx.ex, cy = (e / bx.ex) % bx.ey, cz = e / ((int64_t)bx.ex * bx.ey);
+    xoff = ((cz * 7) * ny + cy * 7 + r.fj) * nx + cx * 7 + r.fi;
+    xstr = nx * ny;
+  }
 #pragma unroll 1
   for (int c = 0; c < NCOL; ++c) {
     double xk[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      xk[k] = XLAND ? landing_one<NCOL>()[(k * 64 + lin) * NCOL + c] : __ldg(a.x + (e * N3 + k * 64 + lin) * NCOL + c);
+      xk[k] = XLAND ? landing_one<NCOL>()[(k * 64 + lin) * NCOL + c] : __ldg(a.x + xoff + k * xstr + c);
 #pragma unroll
     for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
     if (TRI && F::kStageA && c == 0) tri_stage_a(t, s_verts[b], s_tri);
@@ -1122,7 +1132,7 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
   // the bulk copies need 16-byte aligned sources
   if (!aligned16(a->x) || (a->verts && !aligned16(a->verts))) return cudaErrorNotSupported;
   const bool helm = a->equation == HX_HELMHOLTZ;
-  const int hook = a->reserved;
+  const int hook = a->gather ? 0 : a->reserved;  // fused gather lives in the single-shot kernels
   if (a->n_col == 3 && hook != 4) {
     switch (a->factor_source) {
       case HX_TRILINEAR:

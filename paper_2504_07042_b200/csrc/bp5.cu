@@ -79,6 +79,49 @@ __global__ void scatter_add_kernel(Box b, const double* __restrict__ yl, double*
   }
 }
 
+// v = mask(Q^T yl) and block partials of p.v over the owned nodes (fused CG step)
+__global__ void scatter_dot_kernel(Box b, const double* __restrict__ yl, double* __restrict__ v,
+                                   const double* __restrict__ p, int64_t n_owned, double* __restrict__ partial) {
+  __shared__ double sred[256];
+  const int n1 = b.order + 1, n3 = n1 * n1 * n1;
+  const int64_t nx = (int64_t)b.ex * b.order + 1, ny = (int64_t)b.ey * b.order + 1;
+  const int64_t nzl = (int64_t)b.nz_el * b.order + 1;
+  const int64_t nz_glob = (int64_t)b.ez * b.order + 1;
+  const int64_t gz_off = (int64_t)b.z0 * b.order;
+  const int64_t total = nx * ny * nzl;
+  double dot = 0.0;
+  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
+       gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gx = gid % nx, gy = (gid / nx) % ny, gz = gid / (nx * ny);
+    double acc = 0.0;
+    const int64_t gzg = gz + gz_off;
+    const bool boundary = gx == 0 || gx == nx - 1 || gy == 0 || gy == ny - 1 || gzg == 0 || gzg == nz_glob - 1;
+    if (!boundary) {
+      int64_t cxs[2], cys[2], czs[2];
+      int ls_x[2], ls_y[2], ls_z[2];
+      const int nxo = axis_owners(gx, b.order, b.ex, cxs, ls_x);
+      const int nyo = axis_owners(gy, b.order, b.ey, cys, ls_y);
+      const int nzo = axis_owners(gz, b.order, b.nz_el, czs, ls_z);
+      for (int a = 0; a < nzo; ++a)
+        for (int bb = 0; bb < nyo; ++bb)
+          for (int c = 0; c < nxo; ++c) {
+            const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
+            const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
+            acc += yl[(e * n3 + node) * b.n_col + b.col];
+          }
+    }
+    v[gid] = acc;
+    if (gid < n_owned) dot = fma(p[gid], acc, dot);
+  }
+  sred[threadIdx.x] = dot;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sred[threadIdx.x] += sred[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sred[0];
+}
+
 // zero the physical boundary of the global box (solver.py:56-61, mesh.py:316-335)
 __global__ void mask_kernel(Box b, double* __restrict__ v) {
   const int64_t nx = (int64_t)b.ex * b.order + 1, ny = (int64_t)b.ey * b.order + 1;
@@ -137,6 +180,29 @@ __global__ void cg_xr_kernel(const double* __restrict__ scal, double* __restrict
   }
 }
 
+// x += alpha p; r -= alpha ap; block partials of r.r over the owned nodes
+__global__ void cg_xr_dot_kernel(const double* __restrict__ scal, double* __restrict__ x,
+                                 const double* __restrict__ p, double* __restrict__ r,
+                                 const double* __restrict__ ap, int64_t n, int64_t n_owned,
+                                 double* __restrict__ partial) {
+  __shared__ double sred[256];
+  const double alpha = scal[0] / scal[1];
+  double dot = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
+    r[i] = ri;
+    if (i < n_owned) dot = fma(ri, ri, dot);
+  }
+  sred[threadIdx.x] = dot;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sred[threadIdx.x] += sred[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sred[0];
+}
+
 // p = r + (rr_new / rr) p   (solver.py:170)
 __global__ void cg_p_kernel(const double* __restrict__ scal, double* __restrict__ p, const double* __restrict__ r,
                             int64_t n) {
@@ -191,3 +257,18 @@ extern "C" cudaError_t hx_cg_p_impl(const double* scal, double* p, const double*
   return cudaGetLastError();
 }
 
+
+extern "C" cudaError_t hx_bp5_scatter_dot_impl(Box b, const double* yl, double* v, const double* p, int64_t n_owned,
+                                               double* work, double* out, cudaStream_t s) {
+  hx::bp5::scatter_dot_kernel<<<hx::bp5::kDotBlocks, 256, 0, s>>>(b, yl, v, p, n_owned, work);
+  hx::bp5::dot_final_kernel<<<1, hx::bp5::kDotThreads, 0, s>>>(work, out);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t hx_cg_xr_dot_impl(const double* scal, double* x, const double* p, double* r,
+                                         const double* ap, int64_t n, int64_t n_owned, double* work, double* out,
+                                         cudaStream_t s) {
+  hx::bp5::cg_xr_dot_kernel<<<hx::bp5::kDotBlocks, 256, 0, s>>>(scal, x, p, r, ap, n, n_owned, work);
+  hx::bp5::dot_final_kernel<<<1, hx::bp5::kDotThreads, 0, s>>>(work, out);
+  return cudaGetLastError();
+}

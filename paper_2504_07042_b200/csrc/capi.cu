@@ -48,6 +48,10 @@ cudaError_t hx_bp5_mask_impl(hx_box, double*, cudaStream_t);
 cudaError_t hx_dot_impl(const double*, const double*, int64_t, int64_t, double*, double*, cudaStream_t);
 cudaError_t hx_cg_xr_impl(const double*, double*, const double*, double*, const double*, int64_t, cudaStream_t);
 cudaError_t hx_cg_p_impl(const double*, double*, const double*, int64_t, cudaStream_t);
+cudaError_t hx_bp5_scatter_dot_impl(hx_box, const double*, double*, const double*, int64_t, double*, double*,
+                                    cudaStream_t);
+cudaError_t hx_cg_xr_dot_impl(const double*, double*, const double*, double*, const double*, int64_t, int64_t,
+                              double*, double*, cudaStream_t);
 }
 
 namespace {
@@ -150,6 +154,13 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
   }
   if (!helm && (a->lam0 || a->lam1))
     return fail(HX_ERR_INVALID, "coefficient fields apply to the Helmholtz operator only");
+  if (a->gather) {
+    const hx_box& b = a->gather_box;
+    if (a->order != 7 || a->n_col != 1 || b.order != 7)
+      return fail(HX_ERR_UNSUPPORTED, "fused lattice gather needs order 7 and n_col 1");
+    if ((int64_t)b.ex * b.ey * b.nz_el != a->n_elements) return fail(HX_ERR_INVALID, "gather box / element mismatch");
+    if (a->kernel == 1) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the generic kernel");
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n1 = a->order + 1;
   if (a->kernel != 1) {
@@ -268,4 +279,21 @@ extern "C" int hx_cg_update_p(const double* scal, double* p, const double* r, in
   g_last_error.clear();
   if (!scal || !p || !r || n < 0) return fail(HX_ERR_INVALID, "bad arguments");
   return cuda_status(hx_cg_p_impl(scal, p, r, n, static_cast<cudaStream_t>(stream)), "hx_cg_update_p");
+}
+
+extern "C" int hx_bp5_scatter_dot(const hx_box* box, const double* yl, double* v, const double* p, int64_t n_owned,
+                                  double* work, double* out, void* stream) {
+  g_last_error.clear();
+  if (int st = box_ok(box)) return st;
+  if (!yl || !v || !p || !work || !out) return fail(HX_ERR_INVALID, "null pointer");
+  return cuda_status(hx_bp5_scatter_dot_impl(*box, yl, v, p, n_owned, work, out, static_cast<cudaStream_t>(stream)),
+                     "hx_bp5_scatter_dot");
+}
+
+extern "C" int hx_cg_update_xr_dot(const double* scal, double* x, const double* p, double* r, const double* ap,
+                                   int64_t n, int64_t n_owned, double* work, double* out, void* stream) {
+  g_last_error.clear();
+  if (!scal || !x || !p || !r || !ap || !work || !out || n < 0 || n_owned > n) return fail(HX_ERR_INVALID, "bad arguments");
+  return cuda_status(hx_cg_xr_dot_impl(scal, x, p, r, ap, n, n_owned, work, out, static_cast<cudaStream_t>(stream)),
+                     "hx_cg_update_xr_dot");
 }

@@ -141,6 +141,24 @@ class CudaBackend:
         _native.check(_native.lib().hx_cg_update_p(scal.data_ptr(), p.data_ptr(), r.data_ptr(), p.numel(),
                                                    self._s()))
 
+    # fused CG pieces (single kernels; optional in a backend)
+    def scatter_dot(self, layout, yl, v, p, n_owned, out):
+        b = layout.box()
+        _native.check(_native.lib().hx_bp5_scatter_dot(ctypes.byref(b), yl.data_ptr(), v.data_ptr(), p.data_ptr(),
+                                                       n_owned, self.work.data_ptr(), out.data_ptr(), self._s()))
+
+    def update_xr_dot(self, scal, x, p, r, ap, n_owned, out):
+        _native.check(_native.lib().hx_cg_update_xr_dot(scal.data_ptr(), x.data_ptr(), p.data_ptr(), r.data_ptr(),
+                                                        ap.data_ptr(), x.numel(), n_owned, self.work.data_ptr(),
+                                                        out.data_ptr(), self._s()))
+
+    def local_apply_lattice(self, local_op, layout, u, yl):
+        """y = A Q u with the gather fused into the AxLocal loads, when supported."""
+        if local_op.spec.order != 7 or local_op.spec.n_col != 1:
+            return False
+        local_op.apply_lattice_(u, yl, layout.box())
+        return True
+
 
 # ---------------------------------------------------------------------------
 class GlobalOperator:
@@ -173,9 +191,28 @@ class GlobalOperator:
         shape = (L.n_elements, n3, spec.n_col)
         self._xl = torch.empty(shape, dtype=torch.float64, device=self.device)
         self._yl = torch.empty(shape, dtype=torch.float64, device=self.device)
-        self.seconds_local = 0.0
-        self.seconds_apply = 0.0
+        self._events = []  # (start, after-gather, after-local, end) per apply, read lazily
+        self._t_local = self._t_apply = 0.0
         self.applies = 0
+
+    def _flush_events(self):
+        if self._events:
+            self._events[-1][3].synchronize()
+            for ev in self._events:
+                self._t_local += ev[1].elapsed_time(ev[2]) * 1e-3
+                self._t_apply += ev[0].elapsed_time(ev[3]) * 1e-3
+            self._events = []
+
+    @property
+    def seconds_local(self) -> float:
+        """Cumulative element-local (AxLocal) device time, as the reference keeps it (solver.py:79-99)."""
+        self._flush_events()
+        return self._t_local
+
+    @property
+    def seconds_apply(self) -> float:
+        self._flush_events()
+        return self._t_apply
 
     def _distribute(self, value):
         """Scalars pass through; global nodal arrays are gathered to the slab's elements (solver.py:102-109)."""
@@ -192,7 +229,8 @@ class GlobalOperator:
         return xl[:, :, 0]
 
     def reset_counters(self) -> None:
-        self.seconds_local = self.seconds_apply = 0.0
+        self._flush_events()
+        self._t_local = self._t_apply = 0.0
         self.applies = 0
 
     def new_vector(self):
@@ -205,7 +243,10 @@ class GlobalOperator:
     def columns(self, v):
         return [v] if self.spec.n_col == 1 else [v[c] for c in range(self.spec.n_col)]
 
-    def apply(self, u, out=None):
+    def apply(self, u, out=None, dot_with=None, dot_out=None):
+        """v = Q^T A Q u on the slab (interfaces completed).  With ``dot_with``
+        (single rank, one column) the boundary mask and the dot
+        dot_out = dot_with . v over owned nodes are fused into the scatter."""
         torch = _torch()
         L, B = self.layout, self.backend
         nc = self.spec.n_col
@@ -214,23 +255,32 @@ class GlobalOperator:
         if timing:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
-        for c, uc in enumerate(self.columns(u)):
-            B.gather(L, uc, self._xl, nc, c)
-        if timing:
+        fused_gather = nc == 1 and hasattr(B, "local_apply_lattice")
+        if fused_gather and timing:
             ev[1].record()
-        self.local_op.apply_(self._xl, self._yl)
+        if not (fused_gather and B.local_apply_lattice(self.local_op, L, u, self._yl)):
+            for c, uc in enumerate(self.columns(u)):
+                B.gather(L, uc, self._xl, nc, c)
+            if timing:
+                ev[1].record()
+            self.local_op.apply_(self._xl, self._yl)
         if timing:
             ev[2].record()
-        for c, vc in enumerate(self.columns(v)):
-            B.scatter(L, self._yl, vc, nc, c)
-            self._exchange_interfaces(vc)
+        fused = dot_with is not None
+        if fused:
+            B.scatter_dot(L, self._yl, v, dot_with, L.n_owned, dot_out)
+        else:
+            for c, vc in enumerate(self.columns(v)):
+                B.scatter(L, self._yl, vc, nc, c)
+                self._exchange_interfaces(vc)
         if timing:
             ev[3].record()
-            ev[3].synchronize()
-            self.seconds_local += ev[1].elapsed_time(ev[2]) * 1e-3
-            self.seconds_apply += ev[0].elapsed_time(ev[3]) * 1e-3
+            self._events.append(ev)
         self.applies += 1
         return v
+
+    def can_fuse_cg(self) -> bool:
+        return self.world.size == 1 and self.spec.n_col == 1 and hasattr(self.backend, "scatter_dot")
 
     def _exchange_interfaces(self, v):
         """Complete the shared z-planes: both neighbours end with lower + upper."""
@@ -306,12 +356,18 @@ class _Reducer:
             part = torch.zeros(1, dtype=torch.float64, device=op.device)
             op.backend.dot(ca, cb, n, part)
             self.scal[slot:slot + 1] += part
+        return self.reduce_slot(slot)
+
+    def reduce_slot(self, slot):
+        """Combine a per-rank partial already in scal[slot] across ranks (rank order)."""
+        torch = _torch()
+        w = self.op.world
         if w.size > 1:
-            parts = [torch.zeros(1, dtype=torch.float64, device=op.device) for _ in range(w.size)]
+            parts = [torch.zeros(1, dtype=torch.float64, device=self.op.device) for _ in range(w.size)]
             w.pg.all_gather(parts, self.scal[slot:slot + 1].clone())
             total = parts[0].clone()
             for t in parts[1:]:
-                total = total + t  # rank order
+                total = total + t
             self.scal[slot:slot + 1] = total
         return float(self.scal[slot].item())
 
@@ -345,17 +401,28 @@ def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mas
     history = [1.0]
     converged = False
     iterations = 0
+    fuse = masked and op.can_fuse_cg()
+    fuse_update = hasattr(B, "update_xr_dot") and op.spec.n_col == 1
     for iterations in range(1, max_iter + 1):
-        op.apply(p, out=ap)
-        if masked:
-            op.mask(ap)
-        pap = red.dot(p, ap, 1)
+        if fuse:
+            # ap = M Q^T A Q p and pap = p . ap in one scatter pass
+            op.apply(p, out=ap, dot_with=p, dot_out=red.scal[1:2])
+            pap = float(red.scal[1].item())
+        else:
+            op.apply(p, out=ap)
+            if masked:
+                op.mask(ap)
+            pap = red.dot(p, ap, 1)
         if not math.isfinite(pap):
             raise FloatingPointError("CG broke down: non-finite curvature")
         if pap <= 0.0:
             raise FloatingPointError("CG broke down: operator is not positive definite")
-        B.update_xr(red.scal, x.reshape(-1), p.reshape(-1), r.reshape(-1), ap.reshape(-1))  # alpha = rr / pap
-        rr_new = red.dot(r, r, 2)
+        if fuse_update:
+            B.update_xr_dot(red.scal, x, p, r, ap, L.n_owned, red.scal[2:3])  # alpha = rr / pap
+            rr_new = red.reduce_slot(2)
+        else:
+            B.update_xr(red.scal, x.reshape(-1), p.reshape(-1), r.reshape(-1), ap.reshape(-1))  # alpha = rr / pap
+            rr_new = red.dot(r, r, 2)
         if not math.isfinite(rr_new):
             raise FloatingPointError("CG broke down: non-finite residual")
         rel = math.sqrt(rr_new) / b_norm
