@@ -614,8 +614,9 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
   if (!XLAND && a.gather) {
     const hx_box& bx = a.gather_box;
     const int64_t nx = (int64_t)bx.ex * 7 + 1, ny = (int64_t)bx.ey * 7 + 1;
-    const int64_t cx = e % bx.ex, cy = (e / bx.ex) % bx.ey, cz = e / ((int64_t)bx.ex * bx.ey);
-    xoff = ((cz * 7) * ny + cy * 7 + r.fj) * nx + cx * 7 + r.fi;
+    const unsigned e32 = (unsigned)e, exu = (unsigned)bx.ex, exy = exu * (unsigned)bx.ey;  // 32-bit division
+    const unsigned cz = e32 / exy, rem = e32 - cz * exy, cy = rem / exu, cx = rem - cy * exu;
+    xoff = ((int64_t)(cz * 7) * ny + cy * 7 + r.fj) * nx + cx * 7 + r.fi;
     xstr = nx * ny;
   }
 #pragma unroll 1

@@ -22,25 +22,12 @@ namespace bp5 {
 
 using Box = hx_box;  // include/hx_axlocal.h
 
-__global__ void gather_kernel(Box b, const double* __restrict__ u, double* __restrict__ xl) {
-  const int n1 = b.order + 1, n3 = n1 * n1 * n1;
-  const int64_t nx = (int64_t)b.ex * b.order + 1, ny = (int64_t)b.ey * b.order + 1;
-  const int64_t total = (int64_t)b.ex * b.ey * b.nz_el * n3;
-  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-       gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = gid / n3;
-    const int node = (int)(gid - e * n3);
-    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
-    const int64_t cx = e % b.ex, cy = (e / b.ex) % b.ey, cz = e / ((int64_t)b.ex * b.ey);
-    const int64_t gx = cx * b.order + i, gy = cy * b.order + j, gz = cz * b.order + k;  // slab-relative z
-    xl[gid * b.n_col + b.col] = u[(gz * ny + gy) * nx + gx];
-  }
-}
 
 // per-axis contributing (element, local index) pairs of lattice coordinate g
 __device__ __forceinline__ int axis_owners(int64_t g, int n, int ne, int64_t c[2], int l[2]) {
-  const int64_t q = g / n;
-  const int r = (int)(g - q * n);
+  const int q32 = (int)((unsigned)g / (unsigned)n);  // lattice coordinates fit in 32 bits
+  const int64_t q = q32;
+  const int r = (int)g - q32 * n;
   int cnt = 0;
   if (r == 0) {
     if (q - 1 >= 0 && q - 1 < ne) { c[cnt] = q - 1; l[cnt] = n; ++cnt; }
@@ -53,86 +40,95 @@ __device__ __forceinline__ int axis_owners(int64_t g, int n, int ne, int64_t c[2
   return cnt;
 }
 
-__global__ void scatter_add_kernel(Box b, const double* __restrict__ yl, double* __restrict__ v) {
-  const int n1 = b.order + 1, n3 = n1 * n1 * n1;
-  const int64_t nx = (int64_t)b.ex * b.order + 1, ny = (int64_t)b.ey * b.order + 1;
-  const int64_t nzl = (int64_t)b.nz_el * b.order + 1;
-  const int64_t total = nx * ny * nzl;
-  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-       gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t gx = gid % nx, gy = (gid / nx) % ny, gz = gid / (nx * ny);
-    int64_t cxs[2], cys[2], czs[2];
-    int ls_x[2], ls_y[2], ls_z[2];
-    const int nxo = axis_owners(gx, b.order, b.ex, cxs, ls_x);
-    const int nyo = axis_owners(gy, b.order, b.ey, cys, ls_y);
-    const int nzo = axis_owners(gz, b.order, b.nz_el, czs, ls_z);
-    double acc = 0.0;
-    // ascending element index e = (cz*ey + cy)*ex + cx: cz outer, then cy, then cx
-    for (int a = 0; a < nzo; ++a)
-      for (int bb = 0; bb < nyo; ++bb)
-        for (int c = 0; c < nxo; ++c) {
-          const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
-          const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
-          acc += yl[(e * n3 + node) * b.n_col + b.col];
-        }
-    v[gid] = acc;
-  }
+
+// One lattice row (fixed gy, gz) per block row: the y and z owners are uniform
+// per block, only x needs a (32-bit) division per thread.
+__device__ __forceinline__ double scatter_node(const Box& b, const double* __restrict__ yl, int gx, int nyo,
+                                               const int64_t* cys, const int* ls_y, int nzo, const int64_t* czs,
+                                               const int* ls_z, int n1, int n3) {
+  int64_t cxs[2];
+  int ls_x[2];
+  const int nxo = axis_owners(gx, b.order, b.ex, cxs, ls_x);
+  double acc = 0.0;
+  // ascending element index e = (cz*ey + cy)*ex + cx: cz outer, then cy, then cx (np.bincount order)
+  for (int a = 0; a < nzo; ++a)
+    for (int bb = 0; bb < nyo; ++bb)
+      for (int c = 0; c < nxo; ++c) {
+        const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
+        const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
+        acc += yl[(e * n3 + node) * b.n_col + b.col];
+      }
+  return acc;
 }
 
-// v = mask(Q^T yl) and block partials of p.v over the owned nodes (fused CG step)
-__global__ void scatter_dot_kernel(Box b, const double* __restrict__ yl, double* __restrict__ v,
-                                   const double* __restrict__ p, int64_t n_owned, double* __restrict__ partial) {
-  __shared__ double sred[256];
+__global__ void scatter_rows_kernel(Box b, const double* __restrict__ yl, double* __restrict__ v,
+                                    const double* __restrict__ p, int64_t n_owned, double* __restrict__ partial,
+                                    int do_mask) {
+  __shared__ double sred[128];
   const int n1 = b.order + 1, n3 = n1 * n1 * n1;
-  const int64_t nx = (int64_t)b.ex * b.order + 1, ny = (int64_t)b.ey * b.order + 1;
-  const int64_t nzl = (int64_t)b.nz_el * b.order + 1;
-  const int64_t nz_glob = (int64_t)b.ez * b.order + 1;
-  const int64_t gz_off = (int64_t)b.z0 * b.order;
-  const int64_t total = nx * ny * nzl;
+  const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1;
+  const int gy = blockIdx.y, gz = blockIdx.z;
+  const int gzg = gz + b.z0 * b.order, nzg = b.ez * b.order + 1;
+  int64_t cys[2], czs[2];
+  int ls_y[2], ls_z[2];
+  const int nyo = axis_owners(gy, b.order, b.ey, cys, ls_y);
+  const int nzo = axis_owners(gz, b.order, b.nz_el, czs, ls_z);
+  const bool row_boundary = gy == 0 || gy == ny - 1 || gzg == 0 || gzg == nzg - 1;
+  const int64_t row = ((int64_t)gz * ny + gy) * nx;
   double dot = 0.0;
-  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-       gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t gx = gid % nx, gy = (gid / nx) % ny, gz = gid / (nx * ny);
+  for (int gx = blockIdx.x * blockDim.x + threadIdx.x; gx < nx; gx += gridDim.x * blockDim.x) {
     double acc = 0.0;
-    const int64_t gzg = gz + gz_off;
-    const bool boundary = gx == 0 || gx == nx - 1 || gy == 0 || gy == ny - 1 || gzg == 0 || gzg == nz_glob - 1;
-    if (!boundary) {
-      int64_t cxs[2], cys[2], czs[2];
-      int ls_x[2], ls_y[2], ls_z[2];
-      const int nxo = axis_owners(gx, b.order, b.ex, cxs, ls_x);
-      const int nyo = axis_owners(gy, b.order, b.ey, cys, ls_y);
-      const int nzo = axis_owners(gz, b.order, b.nz_el, czs, ls_z);
-      for (int a = 0; a < nzo; ++a)
-        for (int bb = 0; bb < nyo; ++bb)
-          for (int c = 0; c < nxo; ++c) {
-            const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
-            const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
-            acc += yl[(e * n3 + node) * b.n_col + b.col];
-          }
-    }
-    v[gid] = acc;
-    if (gid < n_owned) dot = fma(p[gid], acc, dot);
+    if (!(do_mask && (row_boundary || gx == 0 || gx == nx - 1)))
+      acc = scatter_node(b, yl, gx, nyo, cys, ls_y, nzo, czs, ls_z, n1, n3);
+    v[row + gx] = acc;
+    if (p && row + gx < n_owned) dot = fma(p[row + gx], acc, dot);
   }
+  if (!partial) return;
   sred[threadIdx.x] = dot;
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
+  for (int w = 64; w > 0; w >>= 1) {
     if (threadIdx.x < w) sred[threadIdx.x] += sred[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) partial[blockIdx.x] = sred[0];
+  if (threadIdx.x == 0) partial[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = sred[0];
+}
+
+// sums the per-row partials in a fixed order (one block)
+__global__ void rows_final_kernel(const double* __restrict__ partial, int64_t count, double* __restrict__ out) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += 256) acc += partial[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
 }
 
 // zero the physical boundary of the global box (solver.py:56-61, mesh.py:316-335)
-__global__ void mask_kernel(Box b, double* __restrict__ v) {
-  const int64_t nx = (int64_t)b.ex * b.order + 1, ny = (int64_t)b.ey * b.order + 1;
-  const int64_t nzl = (int64_t)b.nz_el * b.order + 1;
-  const int64_t nz_glob = (int64_t)b.ez * b.order + 1;
-  const int64_t gz_off = (int64_t)b.z0 * b.order;
-  const int64_t total = nx * ny * nzl;
-  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-       gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t gx = gid % nx, gy = (gid / nx) % ny, gz = gid / (nx * ny) + gz_off;
-    if (gx == 0 || gx == nx - 1 || gy == 0 || gy == ny - 1 || gz == 0 || gz == nz_glob - 1) v[gid] = 0.0;
+__global__ void mask_rows_kernel(Box b, double* __restrict__ v) {
+  const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1;
+  const int gy = blockIdx.y, gz = blockIdx.z;
+  const int gzg = gz + b.z0 * b.order, nzg = b.ez * b.order + 1;
+  const bool row_boundary = gy == 0 || gy == ny - 1 || gzg == 0 || gzg == nzg - 1;
+  const int64_t row = ((int64_t)gz * ny + gy) * nx;
+  for (int gx = blockIdx.x * blockDim.x + threadIdx.x; gx < nx; gx += gridDim.x * blockDim.x)
+    if (row_boundary || gx == 0 || gx == nx - 1) v[row + gx] = 0.0;
+}
+
+// gather with a 3D grid: one element-row (e, j, k) per thread group, no 64-bit division
+__global__ void gather_rows_kernel(Box b, const double* __restrict__ u, double* __restrict__ xl) {
+  const int n1 = b.order + 1, n3 = n1 * n1 * n1;
+  const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1;
+  const int cy = blockIdx.y % b.ey, cz = blockIdx.y / b.ey;  // element row (cy, cz)
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < b.ex * n3; t += gridDim.x * blockDim.x) {
+    const int cx = t / n3, node = t - cx * n3;
+    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+    const int64_t e = ((int64_t)cz * b.ey + cy) * b.ex + cx;
+    const int64_t g = ((int64_t)(cz * b.order + k) * ny + cy * b.order + j) * nx + cx * b.order + i;
+    xl[(e * n3 + node) * b.n_col + b.col] = u[g];
   }
 }
 
@@ -221,21 +217,30 @@ inline unsigned grid_for(int64_t n, int tpb) {
 
 using hx::bp5::Box;
 
+namespace {
+dim3 rows_grid(const Box& b, int tpb, int* blocks_x = nullptr) {
+  const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1, nzl = b.nz_el * b.order + 1;
+  const int bx = (nx + tpb - 1) / tpb;
+  if (blocks_x) *blocks_x = bx;
+  return dim3(bx, ny, nzl);
+}
+}  // namespace
+
 extern "C" cudaError_t hx_bp5_gather_impl(Box b, const double* u, double* xl, cudaStream_t s) {
-  const int64_t n = (int64_t)b.ex * b.ey * b.nz_el * (b.order + 1) * (b.order + 1) * (b.order + 1);
-  hx::bp5::gather_kernel<<<hx::bp5::grid_for(n, 256), 256, 0, s>>>(b, u, xl);
+  const int n3 = (b.order + 1) * (b.order + 1) * (b.order + 1);
+  const int per_row = b.ex * n3;
+  dim3 grid((per_row + 255) / 256, b.ey * b.nz_el);
+  hx::bp5::gather_rows_kernel<<<grid, 256, 0, s>>>(b, u, xl);
   return cudaGetLastError();
 }
 
 extern "C" cudaError_t hx_bp5_scatter_impl(Box b, const double* yl, double* v, cudaStream_t s) {
-  const int64_t n = ((int64_t)b.ex * b.order + 1) * ((int64_t)b.ey * b.order + 1) * ((int64_t)b.nz_el * b.order + 1);
-  hx::bp5::scatter_add_kernel<<<hx::bp5::grid_for(n, 256), 256, 0, s>>>(b, yl, v);
+  hx::bp5::scatter_rows_kernel<<<rows_grid(b, 128), 128, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
   return cudaGetLastError();
 }
 
 extern "C" cudaError_t hx_bp5_mask_impl(Box b, double* v, cudaStream_t s) {
-  const int64_t n = ((int64_t)b.ex * b.order + 1) * ((int64_t)b.ey * b.order + 1) * ((int64_t)b.nz_el * b.order + 1);
-  hx::bp5::mask_kernel<<<hx::bp5::grid_for(n, 256), 256, 0, s>>>(b, v);
+  hx::bp5::mask_rows_kernel<<<rows_grid(b, 128), 128, 0, s>>>(b, v);
   return cudaGetLastError();
 }
 
@@ -258,10 +263,12 @@ extern "C" cudaError_t hx_cg_p_impl(const double* scal, double* p, const double*
 }
 
 
+// work must hold one partial per lattice row block: ceil(nx/128) * ny * nzl doubles
 extern "C" cudaError_t hx_bp5_scatter_dot_impl(Box b, const double* yl, double* v, const double* p, int64_t n_owned,
                                                double* work, double* out, cudaStream_t s) {
-  hx::bp5::scatter_dot_kernel<<<hx::bp5::kDotBlocks, 256, 0, s>>>(b, yl, v, p, n_owned, work);
-  hx::bp5::dot_final_kernel<<<1, hx::bp5::kDotThreads, 0, s>>>(work, out);
+  const dim3 grid = rows_grid(b, 128);
+  hx::bp5::scatter_rows_kernel<<<grid, 128, 0, s>>>(b, yl, v, p, n_owned, work, 1);
+  hx::bp5::rows_final_kernel<<<1, 256, 0, s>>>(work, (int64_t)grid.x * grid.y * grid.z, out);
   return cudaGetLastError();
 }
 

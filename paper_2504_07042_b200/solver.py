@@ -143,9 +143,14 @@ class CudaBackend:
 
     # fused CG pieces (single kernels; optional in a backend)
     def scatter_dot(self, layout, yl, v, p, n_owned, out):
+        torch = _torch()
+        need = -(-layout.nx // 128) * layout.ny * layout.planes
+        if getattr(self, "_row_work", None) is None or self._row_work.numel() < need:
+            self._row_work = torch.empty(need, dtype=torch.float64, device=self.device)
         b = layout.box()
         _native.check(_native.lib().hx_bp5_scatter_dot(ctypes.byref(b), yl.data_ptr(), v.data_ptr(), p.data_ptr(),
-                                                       n_owned, self.work.data_ptr(), out.data_ptr(), self._s()))
+                                                       n_owned, self._row_work.data_ptr(), out.data_ptr(),
+                                                       self._s()))
 
     def update_xr_dot(self, scal, x, p, r, ap, n_owned, out):
         _native.check(_native.lib().hx_cg_update_xr_dot(scal.data_ptr(), x.data_ptr(), p.data_ptr(), r.data_ptr(),
