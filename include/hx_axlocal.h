@@ -195,7 +195,7 @@ int hx_bp5_mask(const hx_box* box, double* v, void* stream);
  *    (the pap of solver.py:152-153; v = ap);
  *  hx_cg_update_xr_dot: x += (rr/pap) p, r -= (rr/pap) ap and *out = sum_{i < n_owned} r[i]^2.
  * Both reduce in a fixed tree; work holds >= 1184 doubles for hx_cg_update_xr_dot and
- * ceil((ex*N+1)/128) * (ey*N+1) * (nz_el*N+1) doubles (one per lattice row block)
+ * ceil((ey*N+1)/16) * (nz_el*N+1) doubles (one per band of 16 lattice rows)
  * for hx_bp5_scatter_dot. */
 int hx_bp5_scatter_dot(const hx_box* box, const double* yl, double* v, const double* p, int64_t n_owned,
                        double* work, double* out, void* stream);

@@ -41,56 +41,65 @@ __device__ __forceinline__ int axis_owners(int64_t g, int n, int ne, int64_t c[2
 }
 
 
-// One lattice row (fixed gy, gz) per block row: the y and z owners are uniform
-// per block, only x needs a (32-bit) division per thread.
-__device__ __forceinline__ double scatter_node(const Box& b, const double* __restrict__ yl, int gx, int nyo,
-                                               const int64_t* cys, const int* ls_y, int nzo, const int64_t* czs,
-                                               const int* ls_z, int n1, int n3) {
-  int64_t cxs[2];
-  int ls_x[2];
-  const int nxo = axis_owners(gx, b.order, b.ex, cxs, ls_x);
-  double acc = 0.0;
-  // ascending element index e = (cz*ey + cy)*ex + cx: cz outer, then cy, then cx (np.bincount order)
-  for (int a = 0; a < nzo; ++a)
-    for (int bb = 0; bb < nyo; ++bb)
-      for (int c = 0; c < nxo; ++c) {
-        const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
-        const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
-        acc += yl[(e * n3 + node) * b.n_col + b.col];
-      }
-  return acc;
-}
 
-__global__ void scatter_rows_kernel(Box b, const double* __restrict__ yl, double* __restrict__ v,
-                                    const double* __restrict__ p, int64_t n_owned, double* __restrict__ partial,
-                                    int do_mask) {
-  __shared__ double sred[128];
-  const int n1 = b.order + 1, n3 = n1 * n1 * n1;
-  const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1;
-  const int gy = blockIdx.y, gz = blockIdx.z;
-  const int gzg = gz + b.z0 * b.order, nzg = b.ez * b.order + 1;
-  int64_t cys[2], czs[2];
-  int ls_y[2], ls_z[2];
-  const int nyo = axis_owners(gy, b.order, b.ey, cys, ls_y);
-  const int nzo = axis_owners(gz, b.order, b.nz_el, czs, ls_z);
-  const bool row_boundary = gy == 0 || gy == ny - 1 || gzg == 0 || gzg == nzg - 1;
-  const int64_t row = ((int64_t)gz * ny + gy) * nx;
+constexpr int kRowsPerBlock = 16;  // a block owns a band of lattice rows (fixed gz)
+
+// NT = compile-time order (7) or 0 (runtime b.order).  Each thread walks one
+// lattice column x = gx through the band's rows: the rows' loads are
+// independent, so several are in flight per thread.
+template <int NT>
+__global__ void __launch_bounds__(256) scatter_band_kernel(Box b, const double* __restrict__ yl,
+                                                           double* __restrict__ v, const double* __restrict__ p,
+                                                           int64_t n_owned, double* __restrict__ partial,
+                                                           int do_mask) {
+  __shared__ double sred[256];
+  const int n = NT ? NT : b.order;
+  const int n1 = n + 1, n3 = n1 * n1 * n1;
+  const int nx = b.ex * n + 1, ny = b.ey * n + 1;
+  const int gz = blockIdx.y;
+  const int gzg = gz + b.z0 * n, nzg = b.ez * n + 1;
+  int64_t czs[2];
+  int ls_z[2];
+  const int nzo = axis_owners(gz, n, b.nz_el, czs, ls_z);
+  const bool plane_boundary = gzg == 0 || gzg == nzg - 1;
+  const int gy0 = blockIdx.x * kRowsPerBlock;
+  const int gy1 = min(gy0 + kRowsPerBlock, ny);
+  const int64_t ncol = b.n_col;
   double dot = 0.0;
-  for (int gx = blockIdx.x * blockDim.x + threadIdx.x; gx < nx; gx += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    if (!(do_mask && (row_boundary || gx == 0 || gx == nx - 1)))
-      acc = scatter_node(b, yl, gx, nyo, cys, ls_y, nzo, czs, ls_z, n1, n3);
-    v[row + gx] = acc;
-    if (p && row + gx < n_owned) dot = fma(p[row + gx], acc, dot);
+  for (int gx = threadIdx.x; gx < nx; gx += blockDim.x) {
+    int64_t cxs[2];
+    int ls_x[2];
+    const int nxo = axis_owners(gx, n, b.ex, cxs, ls_x);
+    const bool col_boundary = plane_boundary || gx == 0 || gx == nx - 1;
+#pragma unroll 4
+    for (int gy = gy0; gy < gy1; ++gy) {
+      int64_t cys[2];
+      int ls_y[2];
+      const int nyo = axis_owners(gy, n, b.ey, cys, ls_y);
+      double acc = 0.0;
+      if (!(do_mask && (col_boundary || gy == 0 || gy == ny - 1))) {
+        // ascending element index e = (cz*ey + cy)*ex + cx (np.bincount order)
+        for (int a = 0; a < nzo; ++a)
+          for (int bb = 0; bb < nyo; ++bb)
+            for (int c = 0; c < nxo; ++c) {
+              const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
+              const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
+              acc += yl[(e * n3 + node) * ncol + b.col];
+            }
+      }
+      const int64_t gid = ((int64_t)gz * ny + gy) * nx + gx;
+      v[gid] = acc;
+      if (p && gid < n_owned) dot = fma(p[gid], acc, dot);
+    }
   }
   if (!partial) return;
   sred[threadIdx.x] = dot;
   __syncthreads();
-  for (int w = 64; w > 0; w >>= 1) {
+  for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w) sred[threadIdx.x] += sred[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) partial[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = sred[0];
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = sred[0];
 }
 
 // sums the per-row partials in a fixed order (one block)
@@ -218,11 +227,13 @@ inline unsigned grid_for(int64_t n, int tpb) {
 using hx::bp5::Box;
 
 namespace {
-dim3 rows_grid(const Box& b, int tpb, int* blocks_x = nullptr) {
+dim3 rows_grid(const Box& b, int tpb) {
   const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1, nzl = b.nz_el * b.order + 1;
-  const int bx = (nx + tpb - 1) / tpb;
-  if (blocks_x) *blocks_x = bx;
-  return dim3(bx, ny, nzl);
+  return dim3((nx + tpb - 1) / tpb, ny, nzl);
+}
+dim3 band_grid(const Box& b) {
+  const int ny = b.ey * b.order + 1, nzl = b.nz_el * b.order + 1;
+  return dim3((ny + hx::bp5::kRowsPerBlock - 1) / hx::bp5::kRowsPerBlock, nzl);
 }
 }  // namespace
 
@@ -235,7 +246,10 @@ extern "C" cudaError_t hx_bp5_gather_impl(Box b, const double* u, double* xl, cu
 }
 
 extern "C" cudaError_t hx_bp5_scatter_impl(Box b, const double* yl, double* v, cudaStream_t s) {
-  hx::bp5::scatter_rows_kernel<<<rows_grid(b, 128), 128, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
+  if (b.order == 7)
+    hx::bp5::scatter_band_kernel<7><<<band_grid(b), 256, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
+  else
+    hx::bp5::scatter_band_kernel<0><<<band_grid(b), 256, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
   return cudaGetLastError();
 }
 
@@ -263,12 +277,15 @@ extern "C" cudaError_t hx_cg_p_impl(const double* scal, double* p, const double*
 }
 
 
-// work must hold one partial per lattice row block: ceil(nx/128) * ny * nzl doubles
+// work must hold one partial per band of rows: ceil(ny/16) * nzl doubles
 extern "C" cudaError_t hx_bp5_scatter_dot_impl(Box b, const double* yl, double* v, const double* p, int64_t n_owned,
                                                double* work, double* out, cudaStream_t s) {
-  const dim3 grid = rows_grid(b, 128);
-  hx::bp5::scatter_rows_kernel<<<grid, 128, 0, s>>>(b, yl, v, p, n_owned, work, 1);
-  hx::bp5::rows_final_kernel<<<1, 256, 0, s>>>(work, (int64_t)grid.x * grid.y * grid.z, out);
+  const dim3 grid = band_grid(b);
+  if (b.order == 7)
+    hx::bp5::scatter_band_kernel<7><<<grid, 256, 0, s>>>(b, yl, v, p, n_owned, work, 1);
+  else
+    hx::bp5::scatter_band_kernel<0><<<grid, 256, 0, s>>>(b, yl, v, p, n_owned, work, 1);
+  hx::bp5::rows_final_kernel<<<1, 256, 0, s>>>(work, (int64_t)grid.x * grid.y, out);
   return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -144,7 +145,7 @@ class CudaBackend:
     # fused CG pieces (single kernels; optional in a backend)
     def scatter_dot(self, layout, yl, v, p, n_owned, out):
         torch = _torch()
-        need = -(-layout.nx // 128) * layout.ny * layout.planes
+        need = -(-layout.ny // 16) * layout.planes
         if getattr(self, "_row_work", None) is None or self._row_work.numel() < need:
             self._row_work = torch.empty(need, dtype=torch.float64, device=self.device)
         b = layout.box()
@@ -157,9 +158,11 @@ class CudaBackend:
                                                         ap.data_ptr(), x.numel(), n_owned, self.work.data_ptr(),
                                                         out.data_ptr(), self._s()))
 
+    fused_gather = os.environ.get("HX_BP5_FUSED_GATHER", "1") != "0"
+
     def local_apply_lattice(self, local_op, layout, u, yl):
         """y = A Q u with the gather fused into the AxLocal loads, when supported."""
-        if local_op.spec.order != 7 or local_op.spec.n_col != 1:
+        if not self.fused_gather or local_op.spec.order != 7 or local_op.spec.n_col != 1:
             return False
         local_op.apply_lattice_(u, yl, layout.box())
         return True
