@@ -120,6 +120,8 @@ struct TriShared {
   double d[12];     // v4-v0, v5-v1, v7-v3, v6-v2
   double t00[8][9];  // K00(j, k): depends on j and k only (padded rows)
   double t11[8][9];  // K11(i, k): depends on i and k only
+  double xs[8];      // GLL points and weights, for thread-dependent indices
+  double ws[8];
 };
 
 __device__ __forceinline__ double dot3(const double* u, const double* v) {
@@ -150,6 +152,10 @@ __device__ __forceinline__ void tri_stage_a(int t, const double* __restrict__ v,
     const int pa = pair == 0 ? 4 : pair == 1 ? 5 : pair == 2 ? 7 : 6;
     const int pb = pair == 0 ? 0 : pair == 1 ? 1 : pair == 2 ? 3 : 2;
     s.d[q] = v[pa * 3 + c] - v[pb * 3 + c];
+  }
+  if (t < 8) {
+    s.xs[t] = xr(t);
+    s.ws[t] = wr(t);
   }
 }
 
@@ -201,7 +207,7 @@ struct TrilinearPoly {
     if (TAB) {
       // this thread's entries: K00(j = fj, k = fi) and K11(i = fi, k = fj)
       TriShared& w = const_cast<TriShared&>(s);
-      const double tk = xr(fi), tj = xr(fj);
+      const double tk = SHARED ? s.xs[fi] : xr(fi), tj = SHARED ? s.xs[fj] : xr(fj);
       double cr[3], cs[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -219,7 +225,7 @@ struct TrilinearPoly {
       k11[2] = dot3(ss, ss);
     }
     if (SHARED) {
-      const double xj = xr(fj), xi = xr(fi);
+      const double xj = s.xs[fj], xi = s.xs[fi];
       const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
       const double w00 = a0j * a0i, w01 = a0j * a1i, w10 = a1j * a0i, w11 = a1j * a1i;
 #pragma unroll
@@ -247,7 +253,7 @@ struct TrilinearPoly {
     det[0] = dot3(br, P);
     det[1] = dot3(br, Q) + dot3(sr, P);
     det[2] = dot3(sr, Q);
-    wji8 = 0.125 * (wr(fj) * wr(fi));
+    wji8 = SHARED ? 0.125 * (s.ws[fj] * s.ws[fi]) : 0.125 * (wr(fj) * wr(fi));
     lam_a = lam_b = nullptr;
     l0v = a.lam0_value;
     l1v = a.lam1_value;
