@@ -98,7 +98,9 @@ typedef struct {
   const double* lam1;
   double lam0_value;
   double lam1_value;
-  int32_t kernel;         /* 0 = best available; 1 = generic slice kernel (test hook) */
+  int32_t kernel;         /* 0 = best measured kernel for (order, factor source);
+                             1 = slice kernel (paper Algorithm 4, every order);
+                             2 = fast kernel (specialised N=7, else order-generic) */
   int32_t reserved;
   /* Optional fused gather (BP5): when gather != 0, x is NOT element-local but
    * the slab lattice vector of gather_box and each element reads its nodes

@@ -87,12 +87,14 @@ _lib = None
 
 
 def _load():
-    if not os.path.exists(LIB_PATH):
+    # HX_AXLOCAL_LIB: an alternative build of the same library (tuning experiments, tools/tune_fastn.sh)
+    path = os.environ.get("HX_AXLOCAL_LIB", LIB_PATH)
+    if not os.path.exists(path):
         raise ImportError(
-            f"CUDA library {LIB_PATH} is missing; build it with `make -j` (or __graft_entry__.build()). "
+            f"CUDA library {path} is missing; build it with `make -j` (or __graft_entry__.build()). "
             "There is no CPU fallback."
         )
-    so = ctypes.CDLL(LIB_PATH)
+    so = ctypes.CDLL(path)
     so.hx_version.restype = ctypes.c_char_p
     so.hx_version.argtypes = []
     so.hx_last_error.restype = ctypes.c_char_p

@@ -218,7 +218,7 @@ class LocalOperator:
         if helm and source is not FactorSource.TRILINEAR_MERGED:
             self._lam0, self._lam0v = self._coeff(lam0, E, n3, dev)
             self._lam1, self._lam1v = self._coeff(lam1, E, n3, dev)
-        self.kernel = 0  # 0 = best available, 1 = generic slice kernel
+        self.kernel = 0  # 0 = best measured, 1 = slice kernel, 2 = fast kernel (hx_axlocal_args.kernel)
 
     # ---- setup helpers -------------------------------------------------
     @staticmethod

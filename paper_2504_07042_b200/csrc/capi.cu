@@ -31,6 +31,23 @@ HX_DECL_GENERIC(13)
 HX_DECL_GENERIC(14)
 HX_DECL_GENERIC(15)
 HX_DECL_GENERIC(16)
+#define HX_DECL_FASTN(n)                                                                      \
+  cudaError_t hx_fastn_launch_##n(const hx_axlocal_args*, cudaStream_t);                     \
+  cudaError_t hx_upload_basis_fastn_##n(int, const double*, const double*, const double*);
+HX_DECL_FASTN(2)
+HX_DECL_FASTN(3)
+HX_DECL_FASTN(4)
+HX_DECL_FASTN(5)
+HX_DECL_FASTN(6)
+HX_DECL_FASTN(7)
+HX_DECL_FASTN(9)
+HX_DECL_FASTN(10)
+HX_DECL_FASTN(11)
+HX_DECL_FASTN(12)
+HX_DECL_FASTN(13)
+HX_DECL_FASTN(14)
+HX_DECL_FASTN(15)
+HX_DECL_FASTN(16)
 cudaError_t hx_upload_basis_setup(int, const double*, const double*, const double*);
 cudaError_t hx_upload_basis_fast(int, const double*, const double*, const double*);
 // specialised kernels (ax_fast.cu): returns cudaErrorNotSupported when no
@@ -81,7 +98,19 @@ const generic_fn kGeneric[hx::kMaxN1 + 1] = {
     hx_generic_launch_16,
 };
 
+// order-generic fast kernels (ax_fastn.cu); n1 = 8 is served by ax_fast.cu
+const generic_fn kFastN[hx::kMaxN1 + 1] = {
+    nullptr,           nullptr,           hx_fastn_launch_2,  hx_fastn_launch_3,  hx_fastn_launch_4,
+    hx_fastn_launch_5, hx_fastn_launch_6, hx_fastn_launch_7,  nullptr,            hx_fastn_launch_9,
+    hx_fastn_launch_10, hx_fastn_launch_11, hx_fastn_launch_12, hx_fastn_launch_13, hx_fastn_launch_14,
+    hx_fastn_launch_15, hx_fastn_launch_16,
+};
+
 const upload_fn kUploads[] = {
+    hx_upload_basis_fastn_2,  hx_upload_basis_fastn_3,  hx_upload_basis_fastn_4,  hx_upload_basis_fastn_5,
+    hx_upload_basis_fastn_6,  hx_upload_basis_fastn_7,  hx_upload_basis_fastn_9,  hx_upload_basis_fastn_10,
+    hx_upload_basis_fastn_11, hx_upload_basis_fastn_12, hx_upload_basis_fastn_13, hx_upload_basis_fastn_14,
+    hx_upload_basis_fastn_15, hx_upload_basis_fastn_16,
     hx_upload_basis_generic_2,  hx_upload_basis_generic_3,  hx_upload_basis_generic_4,  hx_upload_basis_generic_5,
     hx_upload_basis_generic_6,  hx_upload_basis_generic_7,  hx_upload_basis_generic_8,  hx_upload_basis_generic_9,
     hx_upload_basis_generic_10, hx_upload_basis_generic_11, hx_upload_basis_generic_12, hx_upload_basis_generic_13,
@@ -164,9 +193,16 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n1 = a->order + 1;
   if (a->kernel != 1) {
-    cudaError_t e = hx_fast_launch(a, s);
+    cudaError_t e = hx_fast_launch(a, s);  // specialised N = 7
     if (e != cudaErrorNotSupported) return cuda_status(e, "hx_axlocal(fast)");
     (void)cudaGetLastError();
+    // kernel 0 keeps the slice kernel where it measures faster (order 1; order 2 with
+    // on-the-fly trilinear factors: per-element setup dominates, profiles/r01_order_sweep.txt)
+    const bool tri = a->factor_source == HX_TRILINEAR || a->factor_source == HX_TRILINEAR_PARTIAL ||
+                     a->factor_source == HX_TRILINEAR_MERGED;
+    const bool slice_wins = a->order == 1 || (a->order == 2 && tri);
+    if (kFastN[n1] && !a->gather && (a->kernel == 2 || !slice_wins))
+      return cuda_status(kFastN[n1](a, s), "hx_axlocal(fastn)");
   }
   if (n1 < 2) {
     // order must be >= 1 so n1 >= 2 always; kept for clarity

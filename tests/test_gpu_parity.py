@@ -20,7 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("no CUDA device", allow_module_level=True)
 
 DEV = torch.device("cuda", 0)
-KERNELS = (0, 1)  # 0 = best (specialised where available), 1 = generic slice kernel
+KERNELS = (0, 1, 2)  # 0 = best measured, 1 = slice kernel (Algorithm 4), 2 = fast kernel (specialised / order-generic)
 
 
 def _op(c, elements, kernel):

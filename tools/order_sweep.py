@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--orders", default="1,2,3,4,5,6,7,8,9,10,11,12,13,14,15")
     ap.add_argument("--variants", default="trilinear,parallelepiped,stored")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--kernels", default="0", help="0 = best, 1 = slice kernel, 2 = fast kernel; e.g. 0,1,2")
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -48,32 +49,38 @@ def main():
             E = verts.shape[0]
             x = torch.randn((E, n1**3, 1), dtype=torch.float64, device=dev)
             y = torch.empty_like(x)
-            for _ in range(2):
-                op.apply_(x, y)
-            torch.cuda.synchronize()
-            time.sleep(0.2)
-            s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            for _ in range(args.reps):
-                op.apply_(x, y)
-            t.record()
-            t.synchronize()
-            ms = s.elapsed_time(t) / args.reps
-            wc = workload_count(spec, include_dmat_traffic=False)
-            t_model = max((wc.f_ax + wc.f_geo) / FP64, wc.m_bytes / HBM) * E
-            frac = t_model / (ms * 1e-3)
-            gdofs = E * n1**3 / (ms * 1e-3) / 1e9
-            kernel = "specialised" if order == 7 else "generic"
-            row = dict(order=order, variant=var, elements=E, dof=E * n1**3, ms=ms, gdofs=gdofs, roofline_frac=frac,
-                       kernel=kernel)
-            rows.append(row)
-            print(f"N={order:2d} {var:15s} E={E:9d} ({E * n1**3 / 1e6:6.1f} M DOF) {ms:8.3f} ms "
-                  f"{gdofs:7.1f} GDOF/s  {100 * frac:5.1f}% of roofline  [{kernel}]", flush=True)
+            for kern in (int(k) for k in args.kernels.split(",")):
+                op.kernel = kern
+                rows.append(_time(op, x, y, spec, E, order, var, kern, args.reps))
             del op, x, y, verts
             torch.cuda.empty_cache()
     if args.json:
         with open(args.json, "w") as fh:
             json.dump(rows, fh, indent=1)
+
+
+def _time(op, x, y, spec, E, order, var, kern, reps):
+    n1 = order + 1
+    for _ in range(2):
+        op.apply_(x, y)
+    torch.cuda.synchronize()
+    time.sleep(0.2)
+    s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        op.apply_(x, y)
+    t.record()
+    t.synchronize()
+    ms = s.elapsed_time(t) / reps
+    wc = workload_count(spec, include_dmat_traffic=False)
+    t_model = max((wc.f_ax + wc.f_geo) / FP64, wc.m_bytes / HBM) * E
+    frac = t_model / (ms * 1e-3)
+    gdofs = E * n1**3 / (ms * 1e-3) / 1e9
+    kernel = {0: "best", 1: "slice", 2: "specialised" if order == 7 else "fast"}[kern]
+    print(f"N={order:2d} {var:15s} E={E:9d} ({E * n1**3 / 1e6:6.1f} M DOF) {ms:8.3f} ms "
+          f"{gdofs:7.1f} GDOF/s  {100 * frac:5.1f}% of roofline  [{kernel}]", flush=True)
+    return dict(order=order, variant=var, elements=E, dof=E * n1**3, ms=ms, gdofs=gdofs, roofline_frac=frac,
+                kernel=kernel)
 
 
 if __name__ == "__main__":
