@@ -22,8 +22,12 @@ from .mesh import (
     Element,
     ElementKind,
     LocalField,
+    Mesh,
+    MeshFormatError,
     box_mesh,
     element_node_coords,
+    load_mesh,
+    save_mesh,
     make_element,
     parallelepiped_defect,
 )
@@ -45,6 +49,10 @@ __all__ = [
     "Element",
     "ElementKind",
     "LocalField",
+    "Mesh",
+    "MeshFormatError",
+    "load_mesh",
+    "save_mesh",
     "box_mesh",
     "element_node_coords",
     "make_element",

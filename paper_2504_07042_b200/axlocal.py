@@ -8,8 +8,9 @@ hand-written sm_100a kernels in ``_lib/libhx_axlocal.so`` (C ABI in
 ``include/hx_axlocal.h``); there is no CPU fallback.
 
 Inputs beyond the reference's:
-* ``elements`` may also be a ``BoxMesh``, or an (E, 8, 3) fp64 array / torch
-  tensor of vertices (kinds then classified on the GPU with make_element's rule);
+* ``elements`` may also be a ``BoxMesh``, a ``Mesh`` (e.g. from ``load_mesh``),
+  or an (E, 8, 3) fp64 array / torch tensor of vertices (kinds then classified
+  on the GPU with make_element's rule);
 * ``apply`` also takes an (E, n1^3, n_col) or (E, n1^3) fp64 CUDA tensor and then
   returns a CUDA tensor (no host round trip); ``apply_(x, y)`` writes into a
   preallocated output.  A host ``LocalField`` in gives a host ``LocalField`` out
@@ -27,7 +28,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .mesh import BoxMesh, Element, ElementKind, LocalField
+from .mesh import BoxMesh, Element, ElementKind, LocalField, Mesh
 
 __all__ = [
     "Equation",
@@ -231,6 +232,8 @@ class LocalOperator:
             return elements.to(device=dev, dtype=torch.float64).contiguous(), None
         if isinstance(elements, BoxMesh):
             return elements.vertices_device(dev), None
+        if isinstance(elements, Mesh):
+            return torch.as_tensor(elements.vertices, device=dev), set(elements.kinds)
         if isinstance(elements, np.ndarray) and elements.ndim == 3:
             if tuple(elements.shape[1:]) != (8, 3):
                 raise ValueError("vertex array must have shape (E, 8, 3)")

@@ -54,14 +54,28 @@ __global__ void trilinear_setup_kernel(int n1, int64_t E, const double* __restri
 // Physical coordinate c of GLL node (i, j, k) under the trilinear map
 // (element_node_coords, mesh.py:130-137).
 __device__ __forceinline__ double node_coord(const double v[24], const double* xi, int i, int j, int k, int c) {
+  // blend weight 0.125 ((b_k b_j) b_i) (the einsum "kc,jb,ia->kjicba"), then the
+  // reference's `blend @ v` product, which its BLAS evaluates as one FMA chain
+  // over the 8 vertices in order (bitwise-checked against numpy/OpenBLAS)
   const double bi[2] = {1.0 - xi[i], 1.0 + xi[i]};
   const double bj[2] = {1.0 - xi[j], 1.0 + xi[j]};
   const double bk[2] = {1.0 - xi[k], 1.0 + xi[k]};
   double s = 0.0;
-  for (int b = 0; b < 8; ++b) s += 0.125 * (bk[(b >> 2) & 1] * bj[(b >> 1) & 1] * bi[b & 1]) * v[b * 3 + c];
+  for (int b = 0; b < 8; ++b) {
+    const double wgt = __dmul_rn(0.125, __dmul_rn(__dmul_rn(bk[(b >> 2) & 1], bj[(b >> 1) & 1]), bi[b & 1]));
+    s = fma(wgt, v[b * 3 + c], s);
+  }
   return s;
 }
 
+// The collocation derivatives in the reference's own rounding (contractions.py:35-57
+// via discrete_jacobians, geometry.py:237-241: np.einsum optimize=False on a strided
+// coordinate column, which numpy evaluates as a sequential sum of separately rounded
+// products for all three directions; bitwise-checked).  On axis-aligned elements an
+// exact-zero Jacobian entry is c * sum_n D_in up to rounding, and a derivative of
+// a coordinate whose range is small against its magnitude cancels ~10 digits: on
+// C1's 1/512 x 1 x 1 elements either moves the stored factors by ~1e-12 relative
+// unless the summation matches.
 // Stored (general-route) factors: collocation Jacobian + dense inverse
 // (discrete_jacobians + factors_from_jacobians, geometry.py:225-276).
 // One block per element: node coordinates staged in shared memory, then each
@@ -87,9 +101,9 @@ __global__ void stored_setup_kernel(int n1, int64_t E, const double* __restrict_
       const double* X = s_xyz + c * n3;
       double dr = 0.0, ds = 0.0, dt = 0.0;
       for (int n = 0; n < n1; ++n) {
-        dr += c_D[od + i * n1 + n] * X[(k * n1 + j) * n1 + n];
-        ds += c_D[od + j * n1 + n] * X[(k * n1 + n) * n1 + i];
-        dt += c_D[od + k * n1 + n] * X[(n * n1 + j) * n1 + i];
+        dr = __dadd_rn(dr, __dmul_rn(c_D[od + i * n1 + n], X[(k * n1 + j) * n1 + n]));
+        ds = __dadd_rn(ds, __dmul_rn(c_D[od + j * n1 + n], X[(k * n1 + n) * n1 + i]));
+        dt = __dadd_rn(dt, __dmul_rn(c_D[od + k * n1 + n], X[(n * n1 + j) * n1 + i]));
       }
       jac[c][0] = dr;
       jac[c][1] = ds;

@@ -17,6 +17,10 @@ Unlike the reference, a box mesh here is array-backed: vertices live in one
 (E, 8, 3) fp64 array (built vectorised, optionally straight on the GPU),
 ``elements`` and ``local_to_global`` are materialised only on demand — the
 reference's O(E) Python loop cannot build the 1.5 M-element configuration.
+
+``Mesh`` / ``save_mesh`` / ``load_mesh`` read and write the reference's
+plain-text mesh format (mesh.py:185-211, 336-402) byte for byte, array-backed
+as well (tests/test_mesh_io.py checks files written by the reference).
 """
 
 from __future__ import annotations
@@ -38,6 +42,10 @@ __all__ = [
     "element_node_coords",
     "box_mesh",
     "box_corners",
+    "Mesh",
+    "MeshFormatError",
+    "save_mesh",
+    "load_mesh",
 ]
 
 REFERENCE_CUBE = np.array(
@@ -280,3 +288,155 @@ def box_mesh(ex, ey, ez, order, extents=((0.0, 1.0), (0.0, 1.0), (0.0, 1.0)), pe
         raise ValueError("order must be at least 1")
     corners = box_corners(ex, ey, ez, extents, perturbation, seed)
     return BoxMesh(counts=(ex, ey, ez), order=order, corners=corners, perturbation=perturbation)
+
+
+_KIND_BY_NAME = {k.value: k for k in ElementKind}
+
+
+class MeshFormatError(ValueError):
+    """A malformed mesh file (reference mesh.py:336-337)."""
+
+
+@dataclass(frozen=True, eq=False)
+class Mesh:
+    """A conforming hexahedral mesh plus its local-to-global node map (reference mesh.py:185-211).
+
+    Array-backed: ``vertices`` (E, 8, 3) fp64 and ``kinds`` (E,) of ``ElementKind``
+    values; ``elements`` builds the reference's Element tuple on demand.
+    """
+
+    vertices: np.ndarray
+    kinds: tuple
+    order: int
+    local_to_global: np.ndarray
+    global_node_count: int
+    lattice_shape: tuple | None = None
+
+    def __post_init__(self):
+        v = np.ascontiguousarray(self.vertices, dtype=np.float64)
+        if v.ndim != 3 or v.shape[1:] != (8, 3):
+            raise ValueError("vertices must have shape (E, 8, 3)")
+        kinds = tuple(ElementKind(k) for k in self.kinds)
+        if len(kinds) != v.shape[0]:
+            raise ValueError("one kind per element")
+        l2g = np.asarray(self.local_to_global, dtype=np.int64)
+        n3 = (self.order + 1) ** 3
+        if l2g.shape != (v.shape[0], n3):
+            raise ValueError("local_to_global must have shape (E, n1**3)")
+        if l2g.min(initial=0) < 0 or (l2g.size and l2g.max() >= self.global_node_count):
+            raise ValueError("local_to_global entries out of range")
+        object.__setattr__(self, "vertices", v)
+        object.__setattr__(self, "kinds", kinds)
+        object.__setattr__(self, "local_to_global", l2g)
+        if self.lattice_shape is not None:
+            object.__setattr__(self, "lattice_shape", tuple(int(n) for n in self.lattice_shape))
+
+    @classmethod
+    def from_elements(cls, elements, order, local_to_global, global_node_count, lattice_shape=None) -> "Mesh":
+        elements = tuple(elements)
+        verts = np.stack([el.vertices for el in elements]) if elements else np.zeros((0, 8, 3))
+        return cls(verts, tuple(el.kind for el in elements), order, local_to_global, global_node_count, lattice_shape)
+
+    @classmethod
+    def from_box(cls, box: "BoxMesh") -> "Mesh":
+        ppd = _kinds_from_defects(box.vertices)
+        kinds = tuple(ElementKind.PARALLELEPIPED if p else ElementKind.TRILINEAR for p in ppd)
+        return cls(box.vertices, kinds, box.order, box.local_to_global, box.global_node_count, box.lattice_shape)
+
+    @property
+    def n_elements(self) -> int:
+        return self.vertices.shape[0]
+
+    @property
+    def elements(self) -> tuple:
+        return tuple(Element(vertices=self.vertices[e], kind=k) for e, k in enumerate(self.kinds))
+
+    def multiplicity(self) -> np.ndarray:
+        """How many element-local nodes map onto each global node (reference mesh.py:209-211)."""
+        return np.bincount(self.local_to_global.ravel(), minlength=self.global_node_count)
+
+
+def save_mesh(mesh, path) -> None:
+    """Write ``mesh`` (a Mesh or BoxMesh) in the reference's text format (mesh.py:340-353).
+
+    Floats are written with Python's shortest round-trip ``repr`` like the
+    reference, so files are byte-identical and reload bit-exactly.
+    """
+    if isinstance(mesh, BoxMesh):
+        mesh = Mesh.from_box(mesh)
+    lines = ["hosfem-mesh v1", f"order {mesh.order}", f"elements {mesh.n_elements}", f"nodes {mesh.global_node_count}"]
+    if mesh.lattice_shape is not None:
+        lines.append("lattice {} {} {}".format(*mesh.lattice_shape))
+    rows = mesh.vertices.reshape(-1, 3).tolist()
+    for e, kind in enumerate(mesh.kinds):
+        lines.append(f"element {e} {kind.value}")
+        lines.extend(" ".join(map(repr, r)) for r in rows[8 * e : 8 * e + 8])
+    lines.append("connectivity")
+    lines.extend(" ".join(map(str, r)) for r in mesh.local_to_global.tolist())
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def load_mesh(path) -> Mesh:
+    """Parse a mesh written by ``save_mesh`` (either implementation; reference mesh.py:356-402).
+
+    Same acceptance rules and error type (``MeshFormatError``) as the reference.
+    """
+    with open(path) as fh:
+        raw = [ln.strip() for ln in fh if ln.strip()]
+    pos = 0
+
+    def take():
+        nonlocal pos
+        if pos >= len(raw):
+            return ""
+        pos += 1
+        return raw[pos - 1]
+
+    if (raw[0] if raw else None) != "hosfem-mesh v1":
+        raise MeshFormatError("not a hosfem mesh file")
+    pos = 1
+
+    def expect(key):
+        parts = (line := take()).split()
+        if not parts or parts[0] != key:
+            raise MeshFormatError(f"expected '{key}' line, got {line!r}")
+        return parts[1:]
+
+    try:
+        order = int(expect("order")[0])
+        n_elements = int(expect("elements")[0])
+        n_nodes = int(expect("nodes")[0])
+        lattice = None
+        line = take()
+        if line.startswith("lattice"):
+            lattice = tuple(int(v) for v in line.split()[1:4])
+            line = take()
+        verts = np.empty((n_elements, 8, 3))
+        kinds = []
+        for e in range(n_elements):
+            head = line.split()
+            if len(head) != 3 or head[0] != "element" or int(head[1]) != e:
+                raise MeshFormatError(f"malformed element header for element {e}")
+            if head[2] not in _KIND_BY_NAME:
+                raise MeshFormatError(f"unknown element kind {head[2]!r}")
+            kinds.append(_KIND_BY_NAME[head[2]])
+            if pos + 8 > len(raw):
+                raise MeshFormatError(f"truncated vertices for element {e}")
+            block = [r.split() for r in raw[pos : pos + 8]]
+            if any(len(r) != 3 for r in block):
+                raise MeshFormatError(f"malformed vertex line in element {e}")
+            verts[e] = np.array(block, dtype=np.float64)
+            pos += 8
+            line = take()
+        if line != "connectivity":
+            raise MeshFormatError("missing connectivity section")
+        if pos + n_elements > len(raw):
+            raise MeshFormatError("truncated connectivity section")
+        conn = raw[pos : pos + n_elements]
+        l2g = np.array([r.split() for r in conn], dtype=np.int64) if n_elements else np.zeros((0, (order + 1) ** 3))
+    except (IndexError, ValueError) as exc:
+        if isinstance(exc, MeshFormatError):
+            raise
+        raise MeshFormatError(str(exc)) from exc
+    return Mesh(verts, tuple(kinds), order, l2g, n_nodes, lattice)

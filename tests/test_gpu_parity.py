@@ -109,6 +109,27 @@ def test_parallelepiped_sheared_box(order, kernel):
         assert O.rel_diff(got, want_st) <= 1e-12
 
 
+@pytest.mark.parametrize("order", [3, 7])
+def test_c1_high_aspect_stored_setup(order):
+    """C1 (box_mesh(512,1,1,N), elements 1/512 x 1 x 1).  Exact-zero Jacobian entries
+    come out of the collocation derivative as rounding noise that the aspect ratio
+    amplifies to ~1e-12 of the output (the reference's own stored and parallelepiped
+    routes differ by 7.6e-12 here, and numpy/BLAS builds differ at that level).  The
+    setup kernel reproduces the reference's rounding of node coordinates and
+    derivatives, so it matches the reference's own run (tests/golden/golden_c1.npz,
+    every 8th element) to 1e-12."""
+    import os
+
+    fx = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_c1.npz"))
+    verts = hx.box_mesh(512, 1, 1, order).vertices
+    x = np.random.default_rng(0).standard_normal((512, (order + 1) ** 3, 1))
+    for src in ("stored", "parallelepiped"):
+        op = hx.LocalOperator(hx.KernelSpec("poisson", 1, src, order), torch.as_tensor(verts, device=DEV),
+                              hx.SpectralBasis.build(order))
+        got = op.apply(torch.as_tensor(x, device=DEV)).cpu().numpy()
+        assert O.rel_diff(got[::8], fx[f"n{order}_{src}"]) <= TOL, src
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_ncol3_bitwise_equals_three_ncol1(kernel):
     """test_axlocal.py:206-225: factor reuse must not change per-column bits."""

@@ -89,3 +89,17 @@ def test_mutation_is_detected(golden):
     y = O.apply(c["source"], c["equation"], c["order"], c["verts"], c["x"], c["lam0"], c["lam1"])
     bad = y * (1 + 1e-6)
     assert O.rel_diff(bad, c["y"]) > 1e-12
+
+
+@pytest.mark.parametrize("order", [3, 7])
+def test_oracle_c1_fixture(order):
+    """C1 (512 x 1 x 1 high-aspect box) against the reference's own run: ppd to
+    round-off; stored within the level at which numpy / BLAS builds differ on this
+    ill-conditioned input (bitwise in the build container)."""
+    import os
+
+    fx = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_c1.npz"))
+    verts = O.box_vertices(512, 1, 1, 0.0, 0)
+    x = np.random.default_rng(0).standard_normal((512, (order + 1) ** 3, 1))[::8]
+    assert O.rel_diff(O.apply("parallelepiped", "poisson", order, verts[::8], x), fx[f"n{order}_parallelepiped"]) <= 1e-14
+    assert O.rel_diff(O.apply("stored", "poisson", order, verts[::8], x), fx[f"n{order}_stored"]) <= 2e-11
