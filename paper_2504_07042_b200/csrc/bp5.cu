@@ -23,30 +23,43 @@ namespace bp5 {
 using Box = hx_box;  // include/hx_axlocal.h
 
 
-// per-axis contributing (element, local index) pairs of lattice coordinate g
-__device__ __forceinline__ int axis_owners(int64_t g, int n, int ne, int64_t c[2], int l[2]) {
-  const int q32 = (int)((unsigned)g / (unsigned)n);  // lattice coordinates fit in 32 bits
-  const int64_t q = q32;
-  const int r = (int)g - q32 * n;
-  int cnt = 0;
+// The (up to two) element copies of lattice coordinate g along one axis, lower
+// element first: element q-1 at local index n and element q at local index 0 when
+// g = q n (a shared plane), else element q at local g - q n.  off = that copy's
+// contribution to the element-local address (element index x stride + local x
+// node stride), so a node's copy address is a sum of three per-axis offsets.
+struct AxisCopies {
+  int64_t off[2];
+  bool ok[2];
+};
+
+__device__ __forceinline__ AxisCopies axis_copies(int g, int n, int ne, int64_t elem_stride, int node_stride) {
+  const int q = (int)((unsigned)g / (unsigned)n);  // lattice coordinates fit in 32 bits
+  const int r = g - q * n;
+  AxisCopies a;
   if (r == 0) {
-    if (q - 1 >= 0 && q - 1 < ne) { c[cnt] = q - 1; l[cnt] = n; ++cnt; }
-    if (q < ne) { c[cnt] = q; l[cnt] = 0; ++cnt; }
+    a.ok[0] = q >= 1 && q - 1 < ne;
+    a.off[0] = (int64_t)(q - 1) * elem_stride + (int64_t)n * node_stride;
+    a.ok[1] = q < ne;
+    a.off[1] = (int64_t)q * elem_stride;
   } else {
-    c[0] = q;
-    l[0] = r;
-    cnt = 1;
+    a.ok[0] = false;
+    a.off[0] = 0;
+    a.ok[1] = true;
+    a.off[1] = (int64_t)q * elem_stride + (int64_t)r * node_stride;
   }
-  return cnt;
+  return a;
 }
 
-
-
 constexpr int kRowsPerBlock = 16;  // a block owns a band of lattice rows (fixed gz)
+constexpr int kDotBlocks = 1184;   // fixed grids: the reduction trees never change
+constexpr int kDotThreads = 256;
 
 // NT = compile-time order (7) or 0 (runtime b.order).  Each thread walks one
-// lattice column x = gx through the band's rows: the rows' loads are
-// independent, so several are in flight per thread.
+// lattice column x = gx through the band's rows; copies are summed z-lower,
+// y-lower, x-lower first (ascending element index, np.bincount's order).  All
+// per-axis state lives in registers (no local-memory arrays), and the rows'
+// loads are independent so several rows are in flight per thread.
 template <int NT>
 __global__ void __launch_bounds__(256) scatter_band_kernel(Box b, const double* __restrict__ yl,
                                                            double* __restrict__ v, const double* __restrict__ p,
@@ -58,34 +71,27 @@ __global__ void __launch_bounds__(256) scatter_band_kernel(Box b, const double* 
   const int nx = b.ex * n + 1, ny = b.ey * n + 1;
   const int gz = blockIdx.y;
   const int gzg = gz + b.z0 * n, nzg = b.ez * n + 1;
-  int64_t czs[2];
-  int ls_z[2];
-  const int nzo = axis_owners(gz, n, b.nz_el, czs, ls_z);
+  const int64_t ncol = b.n_col;
+  const int64_t ex_n3 = (int64_t)b.ex * n3;
+  const AxisCopies az = axis_copies(gz, n, b.nz_el, (int64_t)b.ey * ex_n3, n1 * n1);
   const bool plane_boundary = gzg == 0 || gzg == nzg - 1;
   const int gy0 = blockIdx.x * kRowsPerBlock;
   const int gy1 = min(gy0 + kRowsPerBlock, ny);
-  const int64_t ncol = b.n_col;
   double dot = 0.0;
   for (int gx = threadIdx.x; gx < nx; gx += blockDim.x) {
-    int64_t cxs[2];
-    int ls_x[2];
-    const int nxo = axis_owners(gx, n, b.ex, cxs, ls_x);
+    const AxisCopies ax = axis_copies(gx, n, b.ex, n3, 1);
     const bool col_boundary = plane_boundary || gx == 0 || gx == nx - 1;
 #pragma unroll 4
     for (int gy = gy0; gy < gy1; ++gy) {
-      int64_t cys[2];
-      int ls_y[2];
-      const int nyo = axis_owners(gy, n, b.ey, cys, ls_y);
+      const AxisCopies ay = axis_copies(gy, n, b.ey, ex_n3, n1);
       double acc = 0.0;
       if (!(do_mask && (col_boundary || gy == 0 || gy == ny - 1))) {
-        // ascending element index e = (cz*ey + cy)*ex + cx (np.bincount order)
-        for (int a = 0; a < nzo; ++a)
-          for (int bb = 0; bb < nyo; ++bb)
-            for (int c = 0; c < nxo; ++c) {
-              const int64_t e = (czs[a] * b.ey + cys[bb]) * b.ex + cxs[c];
-              const int node = (ls_z[a] * n1 + ls_y[bb]) * n1 + ls_x[c];
-              acc += yl[(e * n3 + node) * ncol + b.col];
-            }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // ascending element index: z, y, x lower copy first
+          const int iz = q >> 2, iy = (q >> 1) & 1, ix = q & 1;
+          if (az.ok[iz] && ay.ok[iy] && ax.ok[ix])
+            acc += __ldg(yl + (az.off[iz] + ay.off[iy] + ax.off[ix]) * ncol + b.col);
+        }
       }
       const int64_t gid = ((int64_t)gz * ny + gy) * nx + gx;
       v[gid] = acc;
@@ -140,9 +146,6 @@ __global__ void gather_rows_kernel(Box b, const double* __restrict__ u, double* 
     xl[(e * n3 + node) * b.n_col + b.col] = u[g];
   }
 }
-
-constexpr int kDotBlocks = 1184;  // fixed grid: the reduction tree never changes
-constexpr int kDotThreads = 256;
 
 // Block partial sums of a*b over [lo, hi) (fixed strided order, fixed tree).
 __global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t lo,

@@ -269,6 +269,10 @@ int box_ok(const hx_box* b) {
   if (!order_ok(b->order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (b->ex < 1 || b->ey < 1 || b->nz_el < 1 || b->ez < 1 || b->z0 < 0 || b->z0 + b->nz_el > b->ez)
     return fail(HX_ERR_INVALID, "bad box / slab extents");
+  // lattice coordinates and slab element indices are 32-bit in the BP5 kernels
+  if ((int64_t)b->ex * b->ey * b->nz_el > 0x7fffffffLL || (int64_t)b->ex * b->order + 1 > 0x7fffffffLL ||
+      (int64_t)b->ey * b->order + 1 > 0x7fffffffLL || (int64_t)b->ez * b->order + 1 > 0x7fffffffLL)
+    return fail(HX_ERR_UNSUPPORTED, "box too large for 32-bit element / lattice indices");
   if ((b->n_col != 1 && b->n_col != 3) || b->col < 0 || b->col >= b->n_col)
     return fail(HX_ERR_INVALID, "bad column selection");
   return HX_OK;

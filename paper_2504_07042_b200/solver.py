@@ -145,7 +145,7 @@ class CudaBackend:
     # fused CG pieces (single kernels; optional in a backend)
     def scatter_dot(self, layout, yl, v, p, n_owned, out):
         torch = _torch()
-        need = -(-layout.ny // 16) * layout.planes
+        need = -(-layout.ny // 16) * layout.planes  # one partial per band of 16 lattice rows (hx_axlocal.h)
         if getattr(self, "_row_work", None) is None or self._row_work.numel() < need:
             self._row_work = torch.empty(need, dtype=torch.float64, device=self.device)
         b = layout.box()
