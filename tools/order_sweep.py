@@ -2,6 +2,11 @@
 
     python tools/order_sweep.py [--dof 1e8] [--variants trilinear,parallelepiped,stored]
 
+With --cpu (default on) the reference algorithm (CPU oracle port, all host
+threads) is timed beside each (order, variant) on a sample of the same mesh's
+elements (sized for ~0.3 s of CPU work) and the GPU result is checked against
+it on that sample (rel_diff, the reference's metric).
+
 Mesh per order: e^3 elements with e = round((dof / n1^3)^(1/3)), trilinear =
 box_mesh(e,e,e,N, pert 0.1, seed 0), parallelepiped = the unperturbed box under a global
 shear.  Prints GDOF/s and the fraction of the per-variant roofline (reference work model,
@@ -31,6 +36,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kernels", default="0", help="0 = best, 1 = slice kernel, 2 = fast kernel; e.g. 0,1,2")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference timing / parity sample")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     shear = torch.tensor([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]], dtype=torch.float64, device=dev)
@@ -52,11 +58,38 @@ def main():
             for kern in (int(k) for k in args.kernels.split(",")):
                 op.kernel = kern
                 rows.append(_time(op, x, y, spec, E, order, var, kern, args.reps))
+                if not args.no_cpu:
+                    rows[-1].update(_cpu(var, order, verts, x, y))
+                    r = rows[-1]
+                    print(f"        CPU[{r['cpu_threads']}t] {r['cpu_gdofs']:.4f} GDOF/s on {r['cpu_sample']} elements "
+                          f"-> GPU x{r['gdofs'] / r['cpu_gdofs']:.0f}; rel_diff {r['rel_diff']:.1e}", flush=True)
             del op, x, y, verts
             torch.cuda.empty_cache()
     if args.json:
         with open(args.json, "w") as fh:
             json.dump(rows, fh, indent=1)
+
+
+def _cpu(var, order, verts, x, y):
+    """Reference algorithm (oracle port, all host threads) on an element sample + parity on it."""
+    import os
+
+    from oracle import hosfem_oracle as O
+
+    n1 = order + 1
+    threads = os.cpu_count() or 1
+    sample = int(max(threads, min(verts.shape[0], 4e6 // n1**3)))  # ~4 M DOF: ~0.1-0.5 s
+    idx = torch.linspace(0, verts.shape[0] - 1, sample, device=verts.device).long()
+    v = verts[idx].cpu().numpy()
+    xs = x[idx].cpu().numpy()
+    st = O.setup(var, "poisson", order, v)
+    best = float("inf")
+    for _ in range(2):
+        t0 = time.perf_counter()
+        want = O.apply_setup(st, xs, threads=threads)
+        best = min(best, time.perf_counter() - t0)
+    return dict(cpu_gdofs=sample * n1**3 / best / 1e9, cpu_threads=threads, cpu_sample=sample,
+                rel_diff=O.rel_diff(y[idx].cpu().numpy(), want))
 
 
 def _time(op, x, y, spec, E, order, var, kern, reps):
