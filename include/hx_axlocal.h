@@ -100,7 +100,8 @@ typedef struct {
   double lam1_value;
   int32_t kernel;         /* 0 = best measured kernel for (order, factor source);
                              1 = slice kernel (paper Algorithm 4, every order);
-                             2 = fast kernel (specialised N=7, else order-generic) */
+                             2 = fast kernel (specialised N=7, else order-generic);
+                             3 = element-per-thread kernel (orders 1, 2 only) */
   int32_t reserved;
   /* Optional fused gather (BP5): when gather != 0, x is NOT element-local but
    * the slab lattice vector of gather_box and each element reads its nodes

@@ -48,6 +48,10 @@ HX_DECL_FASTN(13)
 HX_DECL_FASTN(14)
 HX_DECL_FASTN(15)
 HX_DECL_FASTN(16)
+cudaError_t hx_low_launch_2(const hx_axlocal_args*, cudaStream_t);
+cudaError_t hx_low_launch_3(const hx_axlocal_args*, cudaStream_t);
+cudaError_t hx_upload_basis_low_2(int, const double*, const double*, const double*);
+cudaError_t hx_upload_basis_low_3(int, const double*, const double*, const double*);
 cudaError_t hx_upload_basis_setup(int, const double*, const double*, const double*);
 cudaError_t hx_upload_basis_fast(int, const double*, const double*, const double*);
 // specialised kernels (ax_fast.cu): returns cudaErrorNotSupported when no
@@ -107,6 +111,7 @@ const generic_fn kFastN[hx::kMaxN1 + 1] = {
 };
 
 const upload_fn kUploads[] = {
+    hx_upload_basis_low_2,    hx_upload_basis_low_3,
     hx_upload_basis_fastn_2,  hx_upload_basis_fastn_3,  hx_upload_basis_fastn_4,  hx_upload_basis_fastn_5,
     hx_upload_basis_fastn_6,  hx_upload_basis_fastn_7,  hx_upload_basis_fastn_9,  hx_upload_basis_fastn_10,
     hx_upload_basis_fastn_11, hx_upload_basis_fastn_12, hx_upload_basis_fastn_13, hx_upload_basis_fastn_14,
@@ -192,12 +197,21 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n1 = a->order + 1;
+  // kernel 0 at orders 1-2: the element-per-thread kernel wherever it measures fastest
+  // (every source but stored; stored streams 6 factor fields per node and the
+  // block-per-element kernels coalesce those better; profiles/r01_order_sweep.txt)
+  const bool low_default = a->kernel == 0 && n1 <= 3 && !a->gather && a->factor_source != HX_STORED;
+  if (a->kernel == 3 || low_default) {  // element-per-thread low-order kernel
+    if (n1 > 3) return fail(HX_ERR_UNSUPPORTED, "kernel 3 (element per thread) covers orders 1 and 2");
+    if (a->gather) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the low-order kernel");
+    return cuda_status(n1 == 2 ? hx_low_launch_2(a, s) : hx_low_launch_3(a, s), "hx_axlocal(low)");
+  }
   if (a->kernel != 1) {
     cudaError_t e = hx_fast_launch(a, s);  // specialised N = 7
     if (e != cudaErrorNotSupported) return cuda_status(e, "hx_axlocal(fast)");
     (void)cudaGetLastError();
-    // kernel 0 keeps the slice kernel where it measures faster (order 1; order 2 with
-    // on-the-fly trilinear factors: per-element setup dominates, profiles/r01_order_sweep.txt)
+    // kernel 0 keeps the slice kernel where it measures faster (stored at order 1;
+    // the fused-gather path at orders 1-2; profiles/r01_order_sweep.txt)
     const bool tri = a->factor_source == HX_TRILINEAR || a->factor_source == HX_TRILINEAR_PARTIAL ||
                      a->factor_source == HX_TRILINEAR_MERGED;
     const bool slice_wins = a->order == 1 || (a->order == 2 && tri);

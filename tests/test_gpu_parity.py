@@ -30,10 +30,12 @@ def _op(c, elements, kernel):
     return op
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", KERNELS + (3,))
 @pytest.mark.parametrize("idx", range(n_golden_cases()))
 def test_golden_case(golden, idx, kernel):
     c = golden_case(golden, idx)
+    if kernel == 3 and c["order"] > 2:
+        pytest.skip("kernel 3 (element per thread) covers orders 1 and 2")
     elements = [hx.make_element(v) for v in c["verts"]]
     op = _op(c, elements, kernel)
     got = op.apply(hx.LocalField(c["x"], c["order"])).data
@@ -128,6 +130,45 @@ def test_c1_high_aspect_stored_setup(order):
                               hx.SpectralBasis.build(order))
         got = op.apply(torch.as_tensor(x, device=DEV)).cpu().numpy()
         assert O.rel_diff(got[::8], fx[f"n{order}_{src}"]) <= TOL, src
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_low_order_element_per_thread_kernel(order):
+    """kernel 3: every source / equation / n_col at N = 1, 2 with a ragged element
+    count (130: one full and one partial block), vs the oracle; n_col=3 bitwise =
+    three n_col=1 applies."""
+    mesh = _random_box(order, 13, 5, 2, pert=0.15, seed=order)
+    E, n3 = mesh.n_elements, (order + 1) ** 3
+    rng = np.random.default_rng(11)
+    lam0 = rng.uniform(0.5, 2.0, (E, n3))
+    lam1 = rng.uniform(0.5, 2.0, (E, n3))
+    shear = np.array([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]])
+    ppd = hx.box_mesh(13, 5, 2, order).vertices @ shear.T
+    cases = [("poisson", s, mesh.vertices) for s in ("stored", "trilinear", "trilinear-partial")]
+    cases += [("helmholtz", s, mesh.vertices) for s in ("stored", "trilinear", "trilinear-merged")]
+    cases += [("poisson", "parallelepiped", ppd), ("helmholtz", "parallelepiped", ppd)]
+    for eq, src, verts in cases:
+        kw = {"lam0": lam0, "lam1": lam1} if eq == "helmholtz" else {}
+        x = rng.standard_normal((E, n3, 3))
+        op3 = hx.LocalOperator(hx.KernelSpec(eq, 3, src, order), torch.as_tensor(verts, device=DEV),
+                               hx.SpectralBasis.build(order), **kw)
+        op1 = hx.LocalOperator(hx.KernelSpec(eq, 1, src, order), torch.as_tensor(verts, device=DEV),
+                               hx.SpectralBasis.build(order), **kw)
+        op3.kernel = op1.kernel = 3
+        y3 = op3.apply(torch.as_tensor(x, device=DEV))
+        want = O.apply(src, eq, order, verts, x, kw.get("lam0"), kw.get("lam1"))
+        assert O.rel_diff(y3.cpu().numpy(), want) <= TOL, (eq, src)
+        for c in range(3):
+            y1 = op1.apply(torch.as_tensor(x[:, :, c : c + 1].copy(), device=DEV))
+            assert torch.equal(y3[:, :, c], y1[:, :, 0]), (eq, src, c)
+
+
+def test_low_order_kernel_rejects_higher_orders():
+    mesh = _random_box(3, 2, 2, 2)
+    op = hx.LocalOperator(hx.KernelSpec("poisson", 1, "trilinear", 3), mesh, hx.SpectralBasis.build(3))
+    op.kernel = 3
+    with pytest.raises(ValueError):
+        op.apply(torch.zeros((8, 64, 1), dtype=torch.float64, device=DEV))
 
 
 @pytest.mark.parametrize("kernel", KERNELS)

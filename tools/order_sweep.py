@@ -34,7 +34,7 @@ def main():
     ap.add_argument("--orders", default="1,2,3,4,5,6,7,8,9,10,11,12,13,14,15")
     ap.add_argument("--variants", default="trilinear,parallelepiped,stored")
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--kernels", default="0", help="0 = best, 1 = slice kernel, 2 = fast kernel; e.g. 0,1,2")
+    ap.add_argument("--kernels", default="0", help="0 = best, 1 = slice, 2 = fast, 3 = thread-per-element (N<=2)")
     ap.add_argument("--json", default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference timing / parity sample")
     args = ap.parse_args()
@@ -109,7 +109,7 @@ def _time(op, x, y, spec, E, order, var, kern, reps):
     t_model = max((wc.f_ax + wc.f_geo) / FP64, wc.m_bytes / HBM) * E
     frac = t_model / (ms * 1e-3)
     gdofs = E * n1**3 / (ms * 1e-3) / 1e9
-    kernel = {0: "best", 1: "slice", 2: "specialised" if order == 7 else "fast"}[kern]
+    kernel = {0: "best", 1: "slice", 2: "specialised" if order == 7 else "fast", 3: "thread-per-element"}[kern]
     print(f"N={order:2d} {var:15s} E={E:9d} ({E * n1**3 / 1e6:6.1f} M DOF) {ms:8.3f} ms "
           f"{gdofs:7.1f} GDOF/s  {100 * frac:5.1f}% of roofline  [{kernel}]", flush=True)
     return dict(order=order, variant=var, elements=E, dof=E * n1**3, ms=ms, gdofs=gdofs, roofline_frac=frac,
