@@ -22,7 +22,10 @@ namespace {
 constexpr int N1 = HX_N1;
 constexpr int N3 = N1 * N1 * N1;
 constexpr int TPB = N1 == 2 ? 128 : 64;  // elements (threads) per block
-constexpr int MINB = N1 == 2 ? 4 : 1;    // n1 = 2: 128 registers; n1 = 3 holds 2 x 27 doubles
+// CTAs per SM for the launch bounds (trilinear sources; the others use 7 / 1): n1 = 2
+// caps registers at 128 (70 for the others, 268 vs 211 GDOF/s for ppd at N = 1);
+// n1 = 3 holds 2 x 27 doubles per thread and gets all 255
+constexpr int MINB = N1 == 2 ? 4 : 1;
 constexpr int PAD = N3 | 1;    // odd stride in doubles: conflict-free 64-bit smem accesses
 
 __host__ __device__ constexpr bool tri_src(int src) {
@@ -30,7 +33,7 @@ __host__ __device__ constexpr bool tri_src(int src) {
 }
 
 template <int NCOL, int SRC, bool HELM>
-__global__ void __launch_bounds__(TPB, MINB) ax_low(const hx_axlocal_args a) {
+__global__ void __launch_bounds__(TPB, tri_src(SRC) ? MINB : (N1 == 2 ? 7 : 1)) ax_low(const hx_axlocal_args a) {
   constexpr int VP = 25;  // padded vertex stride (odd: conflict-free)
   __shared__ double s_v[TPB * PAD];                     // x / y of one column
   __shared__ double s_vert[tri_src(SRC) ? TPB * VP : 1];  // the block's vertices (trilinear sources)
