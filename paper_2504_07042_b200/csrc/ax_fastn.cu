@@ -454,7 +454,8 @@ __global__ void __launch_bounds__(NT, MINB) axn(const __grid_constant__ hx_axloc
 
 // register budget per thread -> CTAs per SM the compiler must fit (launch bounds);
 // the per-thread fibre state grows with n1 (~4 n1 doubles live plus the factors)
-constexpr int regs_of(int n) { return n <= 8 ? 128 : n <= 11 ? 168 : n <= 12 ? 200 : 255; }
+// (two CTAs per SM up to n1 = 15; 16 keeps one copy of the D blocks and needs 255)
+constexpr int regs_of(int n) { return n <= 12 ? 128 : n <= 13 ? 168 : n <= 15 ? 128 : 255; }
 #ifdef HX_FASTN_REGS
 constexpr int kRegs = HX_FASTN_REGS;
 #else
