@@ -601,7 +601,7 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
 
 // COPY selects the copy of the D blocks (so two bodies in one kernel do not
 // share constants); XLAND reads x from the single-element TMA landing buffer.
-template <typename F, int NCOL, bool HELM, bool TRI, int COPY = 0, bool XLAND = false>
+template <typename F, int NCOL, bool HELM, bool TRI, int COPY = 0, bool XLAND = false, bool VGLOBAL = false>
 __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict__ ap, int64_t e, int b = 0) {
   const hx_axlocal_args& a = *ap;
   double* sX = s_cubeX;
@@ -613,6 +613,9 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
   const int rb = Ak(r.rk) + Aj(r.rj);  // i-row base (+ n)
   const int cb = Ak(r.ck) + r.ci;      // j-column base (+ Aj(n))
   const int lin = r.fj * 8 + r.fi;     // k-fibre offset in the linear element (+ 64 k)
+  // VGLOBAL: stage A reads the 24 vertex coordinates straight from global memory (L1),
+  // so the CTA needs no vertex staging barrier
+  const double* vsrc = VGLOBAL ? a.verts + e * 24 : s_verts[b];
 
   // element-local x, or (fused BP5 gather) the slab lattice: node (i,j,k) of
   // element (cx,cy,cz) is lattice point (cx N + i, cy N + j, cz N + k)
@@ -633,11 +636,11 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
       xk[k] = XLAND ? landing_one<NCOL>()[(k * 64 + lin) * NCOL + c] : __ldg(a.x + xoff + k * xstr + c);
 #pragma unroll
     for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
-    if (TRI && F::kStageA && c == 0) tri_stage_a(t, s_verts[b], s_tri);
+    if (TRI && F::kStageA && c == 0) tri_stage_a(t, vsrc, s_tri);
     __syncthreads();
 
     F fac;
-    fac.prepare(a, e, s_tri, s_verts[b], r.fi, r.fj);
+    fac.prepare(a, e, s_tri, vsrc, r.fi, r.fj);
 
     // forward: x2 on the k-fibre; x0 on the i-row; x1 on the j-column
     double x2[8];
@@ -738,7 +741,7 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
 
 // One CTA per element (no persistent loop): the body inlines into the kernel
 // and D's even-odd blocks stay __constant__ operands.
-template <typename F, int NCOL, bool HELM, bool TRI, int MINB>
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB, bool VG = false>
 __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlocal_args a) {
   const int64_t e = blockIdx.x;
   // CTAs start in blockIdx order, ~148 x 8 resident at a time: warm L2 for the
@@ -750,9 +753,11 @@ __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlo
       if (TRI) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
     }
   }
-  if (TRI && threadIdx.x < 24) s_verts[0][threadIdx.x] = __ldg(a.verts + e * 24 + threadIdx.x);
-  if (TRI) __syncthreads();
-  element_direct<F, NCOL, HELM, TRI>(&a, e);
+  if (!VG) {
+    if (TRI && threadIdx.x < 24) s_verts[0][threadIdx.x] = __ldg(a.verts + e * 24 + threadIdx.x);
+    if (TRI) __syncthreads();
+  }
+  element_direct<F, NCOL, HELM, TRI, 0, false, VG>(&a, e);
 }
 
 // Two elements per CTA in straight-line code: the second element's x and
@@ -1101,14 +1106,14 @@ cudaError_t launch_n(const hx_axlocal_args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename F, bool HELM, bool TRI, int MINB>
+template <typename F, bool HELM, bool TRI, int MINB, bool VG = false>
 cudaError_t launch_single(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)a.n_elements;
   if (a.n_col == 3)
-    ax8s<F, 3, HELM, TRI, MINB><<<grid, 64, 0, s>>>(a);
+    ax8s<F, 3, HELM, TRI, MINB, VG><<<grid, 64, 0, s>>>(a);
   else
-    ax8s<F, 1, HELM, TRI, MINB><<<grid, 64, 0, s>>>(a);
+    ax8s<F, 1, HELM, TRI, MINB, VG><<<grid, 64, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1161,7 +1166,7 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
       if (helm) {
         if (hook == 1) return launch<TrilinearPoly<true, false, false>, true, true>(*a, s);
         if (hook == 2) return launch_single<TrilinearPoly<true, false, false, true, false, false, true>, true, true, 10>(*a, s);
-        return launch_single<TrilinearPoly<true, false, false>, true, true, 8>(*a, s);
+        return launch_single<TrilinearPoly<true, false, false>, true, true, 8, true>(*a, s);
       }
       switch (hook) {
         case 1: return launch<TrilinearPoly<false, false, false>, false, true>(*a, s);
@@ -1177,16 +1182,18 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
         case 20: return launch_warp<TrilinearPoly<false, false, false, true>, false, true, 15>(*a, s);
         case 25: return launch_single<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 8>(*a, s);
         case 27: return launch_double<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 8>(*a, s);
-        default: return launch_single<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 10>(*a, s);
+        case 30: return launch_single<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 10>(*a, s);
+        // default: vertices read by stage A from L1 (no staging barrier; +1 % under bench conditions)
+        default: return launch_single<TrilinearPoly<false, false, false, true, false, false, true>, false, true, 10, true>(*a, s);
       }
     case HX_TRILINEAR_PARTIAL:
       if (hook == 1) return launch<TrilinearPoly<false, false, true>, false, true>(*a, s);
       if (hook == 2) return launch_single<TrilinearPoly<false, false, true>, false, true, 8>(*a, s);
-      return launch_single<TrilinearPoly<false, false, true, true, false, false, true>, false, true, 10>(*a, s);
+      return launch_single<TrilinearPoly<false, false, true, true, false, false, true>, false, true, 10, true>(*a, s);
     case HX_TRILINEAR_MERGED:
       if (hook == 1) return launch<TrilinearPoly<true, true, false>, true, true>(*a, s);
       if (hook == 2) return launch_single<TrilinearPoly<true, true, false>, true, true, 8>(*a, s);
-      return launch_single<TrilinearPoly<true, true, false, true, false, false, true>, true, true, 10>(*a, s);
+      return launch_single<TrilinearPoly<true, true, false, true, false, false, true>, true, true, 10, true>(*a, s);
     case HX_STORED:
       if (hook == 1)
         return helm ? launch<StoredLoad<true>, true, false>(*a, s) : launch<StoredLoad<false>, false, false>(*a, s);
