@@ -88,7 +88,7 @@ _lib = None
 
 def _load():
     # HX_AXLOCAL_LIB: an alternative build of the same library (tuning experiments, tools/tune_fastn.sh)
-    path = os.environ.get("HX_AXLOCAL_LIB", LIB_PATH)
+    path = os.environ.get("HX_AXLOCAL_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"CUDA library {path} is missing; build it with `make -j` (or __graft_entry__.build()). "

@@ -161,6 +161,7 @@ __device__ __forceinline__ void stage_a(int t, const double* __restrict__ v, Tri
 template <bool HELM, bool MERGED, bool PARTIAL>
 struct TriPoly {
   static constexpr bool kTri = true;
+  static constexpr bool kHelm = HELM;
   double k01[3], k02[2], k12[2], k22, det[3];
   double wji8;
   const double* tab00;
@@ -269,6 +270,7 @@ struct TriPoly {
 template <bool HELM>
 struct StoredN {
   static constexpr bool kTri = false;
+  static constexpr bool kHelm = HELM;
   const double* g;
   const double* gwj;
   const double* lam0;
@@ -304,6 +306,7 @@ struct StoredN {
 template <bool HELM>
 struct PpdN {
   static constexpr bool kTri = false;
+  static constexpr bool kHelm = HELM;
   double h[7];
   double wj, wi;
   const double* lam0;
@@ -455,21 +458,35 @@ __global__ void __launch_bounds__(NT, MINB) axn(const __grid_constant__ hx_axloc
 // register budget per thread -> CTAs per SM the compiler must fit (launch bounds);
 // the per-thread fibre state grows with n1 (~4 n1 doubles live plus the factors)
 // (two CTAs per SM up to n1 = 15; 16 keeps one copy of the D blocks and needs 255)
-constexpr int regs_of(int n) { return n <= 12 ? 128 : n <= 13 ? 168 : n <= 15 ? 128 : 255; }
 #ifdef HX_FASTN_REGS
 constexpr int kRegs = HX_FASTN_REGS;
 #else
+constexpr int regs_of(int n) { return n <= 12 ? 128 : n <= 13 ? 168 : n <= 15 ? 128 : 255; }
 constexpr int kRegs = regs_of(N1);
 #endif
-constexpr int kMinB = 65536 / (NT_WARPS * 32 * kRegs) > 0 ? 65536 / (NT_WARPS * 32 * kRegs) : 1;
+// trilinear sources at n1 <= 7 run best with 80 registers (96 for Helmholtz, which
+// would spill; more CTAs hide the per-element setup: +5-15 % at N = 3-6), the
+// streaming sources keep 128
+template <typename F>
+constexpr int regs_for() {
+#ifdef HX_FASTN_REGS
+  return kRegs;
+#else
+  return F::kTri && N1 <= 7 ? (F::kHelm ? 96 : 80) : kRegs;
+#endif
+}
+template <typename F>
+constexpr int minb_for() {
+  return 65536 / (NT_WARPS * 32 * regs_for<F>()) > 0 ? 65536 / (NT_WARPS * 32 * regs_for<F>()) : 1;
+}
 
 template <typename F, bool HELM>
 cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
   const int64_t blocks = (a.n_elements + EPB - 1) / EPB * a.n_col;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory");
-  auto k1 = axn<F, 1, HELM, kMinB>;
-  auto k3 = axn<F, 3, HELM, kMinB>;
+  auto k1 = axn<F, 1, HELM, minb_for<F>()>;
+  auto k3 = axn<F, 3, HELM, minb_for<F>()>;
   static bool attr = false;
   if (!attr && kSmemBytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
