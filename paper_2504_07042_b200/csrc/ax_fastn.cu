@@ -41,12 +41,18 @@ constexpr int pj_of(int n) {
   return n == 6 ? 9 : n == 8 ? 9 : n == 10 ? 17 : n == 12 ? 13 : n == 14 ? 17 : n == 16 ? 17 : n;
 }
 constexpr int pk_of(int n) {
-  return n == 2 ? 4 : n == 3 ? 12 : n == 4 ? 19 : n == 6 ? 54 : n == 8 ? 72 : n == 10 ? 170 : n == 12 ? 156
-       : n == 14 ? 238 : n == 16 ? 272 : n * n;
+  return n == 2 ? 5 : n == 3 ? 18 : n == 4 ? 19 : n == 6 ? 54 : n == 7 ? 52 : n == 8 ? 72 : n == 10 ? 170
+       : n == 12 ? 156 : n == 14 ? 238 : n == 16 ? 272 : n * n;
 }
 constexpr int PJ = pj_of(N1);
 constexpr int PK = pk_of(N1);
 constexpr int CUBE = (N1 - 1) * PK + (N1 - 1) * PJ + N1;
+// stride between the cubes of the elements packed in one CTA (tools/cube_layout_search.py:
+// PJ, PK and this stride minimise the weighted shared wavefronts of the three fibre
+// patterns over every warp of the CTA; warps straddle elements when n1^2 is not a
+// multiple of 32)
+constexpr int cs_of(int n) { return n == 2 ? 12 : n == 3 ? 57 : n == 5 ? 137 : n == 6 ? 324 : n == 7 ? 369 : 0; }
+constexpr int CS = cs_of(N1) > CUBE ? cs_of(N1) : CUBE;
 
 constexpr int EO = 2 * H * H + 2 * H + 1;  // A[H][H], B[H][H], C[H], R[H], M[mid][mid]
 
@@ -364,16 +370,16 @@ struct NodeLoop<END, END> {
 };
 
 // dynamic shared memory: [X | A | B] cubes per element, then TriShared, then vertices
-constexpr size_t kCubesBytes = sizeof(double) * 3 * EPB * CUBE;
+constexpr size_t kCubesBytes = sizeof(double) * 3 * EPB * CS;
 constexpr size_t kSmemBytes = kCubesBytes + sizeof(TriShared) * EPB + sizeof(double) * 24 * EPB;
 
 template <typename F, int NCOL, bool HELM, int MINB>
 __global__ void __launch_bounds__(NT, MINB) axn(const __grid_constant__ hx_axlocal_args a) {
   extern __shared__ __align__(16) double smem[];
-  double(*sX)[CUBE] = reinterpret_cast<double(*)[CUBE]>(smem);
-  double(*sA)[CUBE] = reinterpret_cast<double(*)[CUBE]>(smem + EPB * CUBE);
-  double(*sB)[CUBE] = reinterpret_cast<double(*)[CUBE]>(smem + 2 * EPB * CUBE);
-  TriShared* sT = reinterpret_cast<TriShared*>(smem + 3 * EPB * CUBE);
+  double(*sX)[CS] = reinterpret_cast<double(*)[CS]>(smem);
+  double(*sA)[CS] = reinterpret_cast<double(*)[CS]>(smem + EPB * CS);
+  double(*sB)[CS] = reinterpret_cast<double(*)[CS]>(smem + 2 * EPB * CS);
+  TriShared* sT = reinterpret_cast<TriShared*>(smem + 3 * EPB * CS);
   double(*sV)[24] = reinterpret_cast<double(*)[24]>(reinterpret_cast<char*>(sT) + sizeof(TriShared) * EPB);
   const int le = threadIdx.x / T, t = threadIdx.x - le * T;
   // n_col = 3: the three columns of an element group are three adjacent CTAs (same

@@ -22,7 +22,7 @@ ap.add_argument("--kernel", type=int, default=0)
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 ex, ey, ez = (int(v) for v in args.mesh.split(","))
-mesh = hx.box_mesh(ex, ey, ez, args.order, perturbation=0.1, seed=0)
+mesh = hx.box_mesh(ex, ey, ez, args.order, perturbation=0.0 if args.source == "parallelepiped" else 0.1, seed=0)
 kw = {"lam0": 1.3, "lam1": 0.4} if args.equation == "helmholtz" else {}
 op = hx.LocalOperator(hx.KernelSpec(args.equation, args.n_col, args.source, args.order), mesh,
                       hx.SpectralBasis.build(args.order), device=dev, **kw)
