@@ -32,7 +32,19 @@ from .mesh import (
     parallelepiped_defect,
 )
 from .workload import WorkloadCount, ax_flops, geo_flops, workload_count
-from .roofline import HardwareProfile, KernelModel, RooflineBounds, load_profile, resolve_profile, roofline_bounds
+from .roofline import (
+    HardwareProfile,
+    KernelModel,
+    RooflineBounds,
+    load_profile,
+    machine_balance,
+    mbp_crossing,
+    measured_performance,
+    operational_intensity,
+    preset_names,
+    resolve_profile,
+    roofline_bounds,
+)
 
 __version__ = "0.1.0"
 
@@ -67,4 +79,9 @@ __all__ = [
     "load_profile",
     "resolve_profile",
     "roofline_bounds",
+    "machine_balance",
+    "mbp_crossing",
+    "measured_performance",
+    "operational_intensity",
+    "preset_names",
 ]

@@ -1,0 +1,6 @@
+"""``python -m paper_2504_07042_b200 {bench,roofline,nekbone}`` (see cli.py)."""
+import sys
+
+from .cli import main
+
+sys.exit(main())

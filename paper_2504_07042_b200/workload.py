@@ -12,7 +12,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-__all__ = ["FP_SIZE", "WorkloadCount", "ax_flops", "geo_flops", "geo_memory_reals", "base_memory_reals", "workload_count"]
+__all__ = ["FP_SIZE", "WorkloadCount", "ax_flops", "geo_flops", "geo_memory_reals", "base_memory_reals",
+           "stored_memory_reals", "workload_count", "matrix_unit_split"]
 
 FP_SIZE = 8
 
@@ -65,6 +66,19 @@ def geo_memory_reals(source, equation, n1: int) -> int:
 def base_memory_reals(equation, n_col: int, n1: int, include_dmat: bool = True) -> int:
     reals = 2 * n_col * n1**3 + (2 * n1**3 if _helm(equation) else 0)
     return reals + (n1**2 if include_dmat else 0)
+
+
+def stored_memory_reals(equation, n_col: int, n1: int) -> int:
+    """Full traffic of the stored-factor baseline in reals (reference workload.py:101-105)."""
+    return base_memory_reals(equation, n_col, n1) + geo_memory_reals("stored", equation, n1)
+
+
+def matrix_unit_split(spec) -> int:
+    """Flops a matrix unit could take: the r and s contractions, forward and
+    transposed, 8 n1^4 per column (reference workload.py:123-127).  On B200 the
+    FP64 matrix path (DMMA) shares the DFMA pipe, so the b200 profile's
+    peak_matrix equals peak_general."""
+    return spec.n_col * 8 * (spec.order + 1) ** 4
 
 
 def workload_count(spec, include_dmat_traffic: bool = True, fp_size: int = FP_SIZE) -> WorkloadCount:
