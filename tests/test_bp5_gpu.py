@@ -90,3 +90,19 @@ def test_cg_is_bitwise_reproducible():
     r2 = S.cg_solve(op, b, tol=1e-8, max_iter=50)
     assert r1.iterations == r2.iterations and r1.residual_history == r2.residual_history
     assert torch.equal(r1.solution, r2.solution)
+
+
+@pytest.mark.parametrize("src", ["trilinear", "stored", "trilinear-partial"])
+def test_fused_gather_is_bitwise_the_unfused_path(src):
+    """The N=7 AxLocal kernels read u straight from the slab lattice (fused gather);
+    the values they see are the gather's, so A Q u is bit-identical either way."""
+    mesh = hx.box_mesh(5, 4, 3, 7, perturbation=0.12, seed=2)
+    op = S.GlobalOperator(mesh, hx.KernelSpec("poisson", 1, src, 7), hx.SpectralBasis.build(7))
+    u = torch.randn(op.layout.n_local, dtype=torch.float64, device=DEV)
+    fused = op.apply(u).clone()
+    op.backend.fused_gather = False
+    try:
+        plain = op.apply(u).clone()
+    finally:
+        op.backend.fused_gather = True
+    assert torch.equal(fused, plain)
