@@ -459,7 +459,16 @@ struct Ppd {
 template <typename F, int K>
 __device__ __forceinline__ void node_at(const F& fac, int n, double x0, double x1, double x2, double& rr,
                                         double& ss, double& tt, double& mass) {
+#if defined(HX_ABLATE) && HX_ABLATE == 1
+  // timing experiment only (tools/build_variant.sh abl1 "-DHX_ABLATE=1" ax_fast; wrong
+  // results): the skeleton without per-node geometry, profiles/r01_ablation_n7.txt
+  rr = x0 * 1.0000001;
+  ss = x1 * 1.0000001;
+  tt = x2 * 1.0000001;
+  mass = 0.0;
+#else
   fac.template node<K>(n, x0, x1, x2, rr, ss, tt, mass);
+#endif
 }
 
 // Shared memory lives at file scope so that the per-element body can be a
