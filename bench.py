@@ -205,6 +205,12 @@ def cpu_sample_baseline(verts, x, sample, budget_s=12.0):
         O.apply_setup(st, xs, threads=threads)
         best = min(best, time.perf_counter() - t0)
         reps += 1
+    # the reference's --threads 1 figure too, on a quarter of the sample
+    s1 = max(1, sample // 4)
+    st1 = O.setup("trilinear", "poisson", ORDER, v[:s1])
+    t0 = time.perf_counter()
+    O.apply_setup(st1, xs[:s1], threads=1)
+    t1 = time.perf_counter() - t0
     dof = sample * (ORDER + 1) ** 3
     return {
         "value": dof / best / 1e9,
@@ -214,7 +220,20 @@ def cpu_sample_baseline(verts, x, sample, budget_s=12.0):
         "sample": f"{sample} elements of the workload mesh (first elements of the slab), trilinear Poisson N=7, "
         f"best of {reps} applies, numpy oracle with {threads} threads (element-range split like axlocal.py:245-257)",
         "seconds_per_apply": best,
+        "value_1thread": s1 * (ORDER + 1) ** 3 / t1 / 1e9,
+        "cpu_model": _cpu_model(),
     }
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def reference_arm(args, world):
@@ -270,6 +289,7 @@ def reference_arm(args, world):
             "sample": f"{sample} elements per step, numpy restatement of hosfem LocalOperator.apply "
             f"(oracle/hosfem_oracle.py) with {threads} threads; the reference is pure Python/numpy "
             "and cannot travel to the GPU box",
+            "cpu_model": _cpu_model(),
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
