@@ -332,8 +332,20 @@ class LocalOperator:
     def apply_(self, x, y, stream=None):
         """y = A x for contiguous fp64 device tensors (E, n1^3, n_col); stream-ordered,
         no allocation, no synchronisation."""
+        self._check_device_pair(x, y)
         self._launch(self._args(x.data_ptr(), y.data_ptr()), stream)
         return y
+
+    def _check_device_pair(self, x, y):
+        torch = _torch()
+        want = (self.n_elements, self.basis.n1**3, self.spec.n_col)
+        for name, t in (("x", x), ("y", y)):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+            if tuple(t.shape) != want and not (t.ndim == 2 and tuple(t.shape) == want[:2] and want[2] == 1):
+                raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {want}")
+            if t.device != self.device:
+                raise ValueError(f"{name} is on {t.device}, the operator on {self.device}")
 
     def _check_shape(self, order, n_el, n_col):
         if order is not None and order != self.spec.order:

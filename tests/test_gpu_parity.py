@@ -296,3 +296,18 @@ def test_mass_limit_reference_cube():
         op = hx.LocalOperator(hx.KernelSpec("helmholtz", 1, src, order), [el], basis, lam0=0.0, lam1=1.0)
         got = op.apply(hx.LocalField(x, order)).data[0, :, 0]
         assert np.abs(got - basis.tensor_weights() * x[0, :, 0]).max() <= 1e-13
+
+
+def test_apply_inplace_validates_buffers():
+    mesh = _random_box(3, 2, 2, 2)
+    op = hx.LocalOperator(hx.KernelSpec("poisson", 1, "trilinear", 3), mesh, hx.SpectralBasis.build(3))
+    x = torch.randn((8, 64, 1), dtype=torch.float64, device=DEV)
+    y = torch.empty_like(x)
+    op.apply_(x, y)
+    assert torch.equal(y, op.apply(x))
+    strided = torch.randn((8, 64, 2), dtype=torch.float64, device=DEV)[:, :, :1]  # not contiguous
+    for bad in (x.float(), x.cpu(), strided, torch.randn((7, 64, 1), dtype=torch.float64, device=DEV)):
+        with pytest.raises(ValueError):
+            op.apply_(bad, y)
+        with pytest.raises(ValueError):
+            op.apply_(x, bad)
