@@ -755,11 +755,24 @@ __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlo
   const int64_t e = blockIdx.x;
   // CTAs start in blockIdx order, ~148 x 8 resident at a time: warm L2 for the
   // element two waves ahead so its CTA's loads do not wait on HBM latency.
-  if (a.reserved != 3 && threadIdx.x == 0) {
+  if (a.reserved != 3) {
     const int64_t ahead = e + kPrefetchAhead;
     if (ahead < a.n_elements) {
-      bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
-      if (TRI) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
+      if (a.gather) {
+        // fused BP5 gather: x is the slab lattice; warm the 64 lattice rows (64 B each)
+        // of the element two waves ahead, one row per thread
+        const hx_box& bx = a.gather_box;
+        const int64_t nx = (int64_t)bx.ex * 7 + 1, ny = (int64_t)bx.ey * 7 + 1;
+        const unsigned e32 = (unsigned)ahead, exu = (unsigned)bx.ex, exy = exu * (unsigned)bx.ey;
+        const unsigned cz = e32 / exy, rem = e32 - cz * exy, cy = rem / exu, cx = rem - cy * exu;
+        const int j = threadIdx.x & 7, k = threadIdx.x >> 3;
+        const double* row = a.x + ((int64_t)(cz * 7 + k) * ny + cy * 7 + j) * nx + cx * 7;
+        prefetch_l2(row);
+        prefetch_l2(row + 7);
+      } else if (threadIdx.x == 0) {
+        bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
+      }
+      if (TRI && threadIdx.x == 0) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
     }
   }
   if (!VG) {
