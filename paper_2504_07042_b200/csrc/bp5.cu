@@ -55,6 +55,43 @@ constexpr int kRowsPerBlock = 16;  // a block owns a band of lattice rows (fixed
 constexpr int kDotBlocks = 1184;   // fixed grids: the reduction trees never change
 constexpr int kDotThreads = 256;
 
+// Blocks start in launch order with ~4 x 148 resident: warm L2 with the element
+// k-planes (512 B each, one bulk prefetch per thread) that the block two waves
+// ahead will read -- the band kernel is otherwise DRAM-latency bound.
+constexpr int64_t kBandAhead = 148 * 4 * 2;
+
+template <int NT>
+__device__ __forceinline__ void prefetch_band_ahead(const Box& b, const double* yl, int nx, int ny) {
+  constexpr int n = NT, n1 = n + 1, n2 = n1 * n1, n3 = n2 * n1;
+  const int64_t nblk = (int64_t)gridDim.x * gridDim.y;
+  const int64_t ahead = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + kBandAhead;
+  if (ahead >= nblk) return;
+  const int band = (int)(ahead % gridDim.x), gz = (int)(ahead / gridDim.x);
+  const int q = gz / n, r = gz - q * n;
+  int cz0, k0, nzc;  // z copies: element layer and k-plane of each
+  if (r == 0) {
+    nzc = (q >= 1 && q - 1 < b.nz_el ? 1 : 0) + (q < b.nz_el ? 1 : 0);
+    cz0 = q >= 1 ? q - 1 : q;
+    k0 = q >= 1 ? n : 0;
+  } else {
+    nzc = 1;
+    cz0 = q;
+    k0 = r;
+  }
+  const int gy0 = band * kRowsPerBlock, gy1 = min(gy0 + kRowsPerBlock, ny);
+  const int cy0 = max(0, gy0 / n - 1), cy1 = min(b.ey - 1, (gy1 - 1) / n);
+  const int ncy = cy1 - cy0 + 1;
+  const int total = nzc * ncy * b.ex;
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int zc = t / (ncy * b.ex), rem = t - zc * ncy * b.ex;
+    const int cy = cy0 + rem / b.ex, cx = rem % b.ex;
+    const int cz = cz0 + zc, kz = zc ? 0 : k0;
+    const int64_t e = ((int64_t)cz * b.ey + cy) * b.ex + cx;
+    bulk_prefetch_l2(yl + e * n3 + (int64_t)kz * n2, n2 * 8);
+  }
+  (void)nx;
+}
+
 // NT = compile-time order (7) or 0 (runtime b.order).  Each thread walks one
 // lattice column x = gx through the band's rows; copies are summed z-lower,
 // y-lower, x-lower first (ascending element index, np.bincount's order).  All
@@ -77,6 +114,9 @@ __global__ void __launch_bounds__(256) scatter_band_kernel(Box b, const double* 
   const bool plane_boundary = gzg == 0 || gzg == nzg - 1;
   const int gy0 = blockIdx.x * kRowsPerBlock;
   const int gy1 = min(gy0 + kRowsPerBlock, ny);
+  if constexpr (NT == 7) {
+    if (ncol == 1) prefetch_band_ahead<NT>(b, yl, nx, ny);
+  }
   double dot = 0.0;
   for (int gx = threadIdx.x; gx < nx; gx += blockDim.x) {
     const AxisCopies ax = axis_copies(gx, n, b.ex, n3, 1);
