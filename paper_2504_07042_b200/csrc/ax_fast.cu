@@ -34,7 +34,10 @@ namespace fast {
 constexpr int N1 = 8;
 constexpr int N3 = 512;
 constexpr int CUBE = 544;  // 543 used
-constexpr int64_t kPrefetchAhead = 2368;  // two waves of 148 SMs x 8 CTAs
+#ifndef HX_PREFETCH_AHEAD
+#define HX_PREFETCH_AHEAD 2368
+#endif
+constexpr int64_t kPrefetchAhead = HX_PREFETCH_AHEAD;  // ~1.6-2 waves of resident CTAs
 
 __host__ __device__ constexpr int Aj(int j) { return 17 * (j >> 1) + 8 * (j & 1); }
 __host__ __device__ constexpr int Ak(int k) { return 68 * k; }
