@@ -1191,7 +1191,9 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
       if (helm) {
         if (hook == 1) return launch<TrilinearPoly<true, false, false>, true, true>(*a, s);
         if (hook == 2) return launch_single<TrilinearPoly<true, false, false, true, false, false, true>, true, true, 10>(*a, s);
-        return launch_single<TrilinearPoly<true, false, false>, true, true, 8, true>(*a, s);
+        if (hook == 3) return launch_single<TrilinearPoly<true, false, false>, true, true, 8, true>(*a, s);
+        // default: K00/K11 tables, vertices from L1, 8 CTAs/SM (10 would spill): +1.4 % over no tables
+        return launch_single<TrilinearPoly<true, false, false, true, false, false, true>, true, true, 8, true>(*a, s);
       }
       switch (hook) {
         case 1: return launch<TrilinearPoly<false, false, false>, false, true>(*a, s);
@@ -1218,6 +1220,7 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
     case HX_TRILINEAR_MERGED:
       if (hook == 1) return launch<TrilinearPoly<true, true, false>, true, true>(*a, s);
       if (hook == 2) return launch_single<TrilinearPoly<true, true, false>, true, true, 8>(*a, s);
+      if (hook == 3) return launch_single<TrilinearPoly<true, true, false, true, false, false, true>, true, true, 8, true>(*a, s);
       return launch_single<TrilinearPoly<true, true, false, true, false, false, true>, true, true, 10, true>(*a, s);
     case HX_STORED:
       if (hook == 1)

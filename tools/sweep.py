@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--only", default=None)
     ap.add_argument("--hook", type=int, default=None, help="run only this tuning hook")
-    ap.add_argument("--pairs", default=None, help="explicit Poisson n_col=1 cases, e.g. trilinear:0,trilinear:30")
+    ap.add_argument("--pairs", default=None, help="explicit n_col=1 cases, e.g. trilinear:0,trilinear:30 "
+                    "(prefix h: for Helmholtz, e.g. h:trilinear:2)")
     args = ap.parse_args()
     ex, ey, ez = (int(v) for v in args.mesh.split(","))
     order = args.order
@@ -66,7 +67,12 @@ def main():
         ("helmholtz", 3, "trilinear-merged", 0, 0),
     ]
     if args.pairs:
-        cases = [("poisson", 1, pr.split(":")[0], 0, int(pr.split(":")[1])) for pr in args.pairs.split(",")]
+        cases = []
+        for pr in args.pairs.split(","):
+            f = pr.split(":")
+            eq = "helmholtz" if f[0] == "h" else "poisson"
+            f = f[1:] if f[0] == "h" else f
+            cases.append((eq, 1, f[0], 0, int(f[1])))
     prepared = []
     for eq, ncol, src, kernel, hook in cases:
         if args.only and args.only not in src:
