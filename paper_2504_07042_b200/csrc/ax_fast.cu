@@ -851,7 +851,7 @@ __device__ __forceinline__ void apply_factors(const double g[6], double sin, dou
   }
 }
 
-template <typename F, bool HELM, bool TRI, int MINB>
+template <typename F, bool HELM, bool TRI, int MINB, bool VG = false>
 __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axlocal_args a) {
   constexpr int NC = 3;
   const int64_t e = blockIdx.x;
@@ -861,8 +861,12 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
   const int rb = Ak(r.rk) + Aj(r.rj);
   const int cb = Ak(r.ck) + r.ci;
   const int lin = r.fj * 8 + r.fi;
-  if (TRI && t < 24) s_verts[0][t] = __ldg(a.verts + e * 24 + t);
-  if (TRI) __syncthreads();
+  // VG: stage A reads the vertices from L1 (no staging barrier)
+  const double* vsrc = VG ? a.verts + e * 24 : s_verts[0];
+  if (!VG) {
+    if (TRI && t < 24) s_verts[0][t] = __ldg(a.verts + e * 24 + t);
+    if (TRI) __syncthreads();
+  }
 
   // P0: the three columns of the k-fibre; x2 = D_t x in registers
   double x2[NC][8];
@@ -875,12 +879,12 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
     for (int k = 0; k < 8; ++k) s_c3X[c][Ak(k) + kp] = xk[k];
     eo8<0>(xk, x2[c]);
   }
-  if (TRI && F::kStageA) tri_stage_a(t, s_verts[0], s_tri);
+  if (TRI && F::kStageA) tri_stage_a(t, vsrc, s_tri);
   __syncthreads();
 
   // P1: forward r (i-rows) and s (j-columns) derivatives of the three columns
   F fac;
-  fac.prepare(a, e, s_tri, s_verts[0], r.fi, r.fj);
+  fac.prepare(a, e, s_tri, vsrc, r.fi, r.fj);
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     double v[8], o[8];
@@ -959,7 +963,10 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
 template <typename F, bool HELM, bool TRI, int MINB = 5>
 cudaError_t launch_c3(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
-  ax8c3<F, HELM, TRI, MINB><<<(unsigned)a.n_elements, 64, 0, s>>>(a);
+  if (TRI && a.reserved == 6)  // vertices from L1: 7 % slower here (profiles/r01_sweep_variants.txt)
+    ax8c3<F, HELM, TRI, MINB, true><<<(unsigned)a.n_elements, 64, 0, s>>>(a);
+  else
+    ax8c3<F, HELM, TRI, MINB><<<(unsigned)a.n_elements, 64, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--only", default=None)
     ap.add_argument("--hook", type=int, default=None, help="run only this tuning hook")
     ap.add_argument("--pairs", default=None, help="explicit n_col=1 cases, e.g. trilinear:0,trilinear:30 "
-                    "(prefix h: for Helmholtz, e.g. h:trilinear:2)")
+                    "(prefix h: for Helmholtz, c3: for n_col=3, e.g. h:c3:trilinear:0)")
     args = ap.parse_args()
     ex, ey, ez = (int(v) for v in args.mesh.split(","))
     order = args.order
@@ -72,7 +72,9 @@ def main():
             f = pr.split(":")
             eq = "helmholtz" if f[0] == "h" else "poisson"
             f = f[1:] if f[0] == "h" else f
-            cases.append((eq, 1, f[0], 0, int(f[1])))
+            ncol = 3 if f[0] == "c3" else 1
+            f = f[1:] if f[0] == "c3" else f
+            cases.append((eq, ncol, f[0], 0, int(f[1])))
     prepared = []
     for eq, ncol, src, kernel, hook in cases:
         if args.only and args.only not in src:
