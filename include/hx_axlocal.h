@@ -119,6 +119,14 @@ const char* hx_version(void);
 const char* hx_last_error(void);
 
 /*
+ * Make `device` the current device of the library's (statically linked) CUDA
+ * runtime for this thread.  Needed before hx_set_basis, whose arguments are host
+ * arrays; every other entry point binds the device owning its first device
+ * pointer itself.
+ */
+int hx_set_device(int32_t device);
+
+/*
  * Upload the GLL basis of one order to the current device's __constant__ bank.
  * points (n1), weights (n1), dmat (n1*n1 row-major, [i][j] = l_j'(x_i)) are HOST
  * arrays from SpectralBasis.build (basis.py:110-136).  Synchronous.  Must be

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 SYMBOLS = (
     "hx_version",
     "hx_last_error",
+    "hx_set_device",
     "hx_set_basis",
     "hx_axlocal",
     "hx_trilinear_validate",
@@ -99,6 +100,8 @@ def _load():
     so.hx_version.argtypes = []
     so.hx_last_error.restype = ctypes.c_char_p
     so.hx_last_error.argtypes = []
+    so.hx_set_device.restype = ctypes.c_int
+    so.hx_set_device.argtypes = [_i32]
     so.hx_set_basis.restype = ctypes.c_int
     so.hx_set_basis.argtypes = [_i32, _c_p, _c_p, _c_p]
     so.hx_axlocal.restype = ctypes.c_int

@@ -117,6 +117,7 @@ def _ensure_basis(device_index: int, basis) -> None:
     wts = np.ascontiguousarray(basis.weights, dtype=np.float64)
     dm = np.ascontiguousarray(basis.diff_matrix, dtype=np.float64)
     with torch.cuda.device(device_index):
+        _native.check(_native.lib().hx_set_device(int(device_index)))
         _native.check(
             _native.lib().hx_set_basis(
                 int(basis.order), pts.ctypes.data, wts.ctypes.data, dm.ctypes.data

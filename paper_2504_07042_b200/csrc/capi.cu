@@ -135,7 +135,29 @@ int cuda_status(cudaError_t e, const char* where) {
 
 bool order_ok(int order) { return order >= 1 && order + 1 <= hx::kMaxN1; }
 
+// The library links the CUDA runtime statically, so its per-thread "current
+// device" is not the host framework's (torch keeps its own runtime's).  Every
+// entry point that takes device memory binds the device owning its first device
+// pointer before launching, so a rank whose framework device is k launches on k.
+int bind_device(const void* p) {
+  if (!p) return HX_OK;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return HX_OK;
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return HX_OK;
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur == at.device) return HX_OK;
+  return cuda_status(cudaSetDevice(at.device), "binding the device of the arguments");
+}
+
 }  // namespace
+
+extern "C" int hx_set_device(int32_t device) {
+  g_last_error.clear();
+  return cuda_status(cudaSetDevice(device), "hx_set_device");
+}
 
 extern "C" const char* hx_version(void) { return HX_VERSION_STRING; }
 
@@ -156,6 +178,7 @@ extern "C" int hx_set_basis(int32_t order, const double* points, const double* w
 extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
   g_last_error.clear();
   if (!a) return fail(HX_ERR_INVALID, "null args");
+  if (int st = bind_device(a->x)) return st;
   if (!order_ok(a->order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (a->n_col != 1 && a->n_col != 3) return fail(HX_ERR_INVALID, "n_col must be 1 or 3");
   if (a->equation != HX_POISSON && a->equation != HX_HELMHOLTZ) return fail(HX_ERR_INVALID, "bad equation");
@@ -228,6 +251,7 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
 extern "C" int hx_trilinear_validate(int32_t order, int64_t E, const double* verts, int64_t* first_bad,
                                      void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(verts)) return st;
   if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (!verts || !first_bad) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_setup_trilinear_impl(order + 1, E, verts, 0, first_bad, nullptr, nullptr, nullptr, 1.0,
@@ -237,6 +261,7 @@ extern "C" int hx_trilinear_validate(int32_t order, int64_t E, const double* ver
 
 extern "C" int hx_setup_partial(int32_t order, int64_t E, const double* verts, double* lam_geo, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(verts)) return st;
   if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (!verts || !lam_geo) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_setup_trilinear_impl(order + 1, E, verts, 1, nullptr, lam_geo, nullptr, nullptr, 1.0,
@@ -247,6 +272,7 @@ extern "C" int hx_setup_partial(int32_t order, int64_t E, const double* verts, d
 extern "C" int hx_setup_merged(int32_t order, int64_t E, const double* verts, const double* lam0, double l0v,
                                const double* lam1, double l1v, double* lam2, double* lam3, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(verts)) return st;
   if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (!verts || !lam2 || !lam3) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_setup_trilinear_impl(order + 1, E, verts, 2, nullptr, lam2, lam3, lam0, l0v, lam1, l1v,
@@ -257,6 +283,7 @@ extern "C" int hx_setup_merged(int32_t order, int64_t E, const double* verts, co
 extern "C" int hx_setup_stored(int32_t order, int64_t E, const double* verts, double* g, double* gwj,
                                int64_t* first_bad, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(verts)) return st;
   if (!order_ok(order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (!verts || !g || !first_bad) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(
@@ -266,6 +293,7 @@ extern "C" int hx_setup_stored(int32_t order, int64_t E, const double* verts, do
 
 extern "C" int hx_setup_parallelepiped(int64_t E, const double* verts, double* h, int64_t* bad, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(verts)) return st;
   if (!verts || !h || !bad) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_setup_ppd_impl(E, verts, h, bad, static_cast<cudaStream_t>(stream)),
                      "hx_setup_parallelepiped");
@@ -273,6 +301,7 @@ extern "C" int hx_setup_parallelepiped(int64_t E, const double* verts, double* h
 
 extern "C" int hx_classify_elements(int64_t E, const double* verts, int8_t* kind, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(verts)) return st;
   if (!verts || !kind) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_classify_impl(E, verts, kind, static_cast<cudaStream_t>(stream)), "hx_classify_elements");
 }
@@ -295,6 +324,7 @@ int box_ok(const hx_box* b) {
 
 extern "C" int hx_bp5_gather(const hx_box* box, const double* u, double* xl, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(u)) return st;
   if (int st = box_ok(box)) return st;
   if (!u || !xl) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_bp5_gather_impl(*box, u, xl, static_cast<cudaStream_t>(stream)), "hx_bp5_gather");
@@ -302,6 +332,7 @@ extern "C" int hx_bp5_gather(const hx_box* box, const double* u, double* xl, voi
 
 extern "C" int hx_bp5_scatter_add(const hx_box* box, const double* yl, double* v, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(yl)) return st;
   if (int st = box_ok(box)) return st;
   if (!yl || !v) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_bp5_scatter_impl(*box, yl, v, static_cast<cudaStream_t>(stream)), "hx_bp5_scatter_add");
@@ -309,6 +340,7 @@ extern "C" int hx_bp5_scatter_add(const hx_box* box, const double* yl, double* v
 
 extern "C" int hx_bp5_mask(const hx_box* box, double* v, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(v)) return st;
   if (int st = box_ok(box)) return st;
   if (!v) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_bp5_mask_impl(*box, v, static_cast<cudaStream_t>(stream)), "hx_bp5_mask");
@@ -317,6 +349,7 @@ extern "C" int hx_bp5_mask(const hx_box* box, double* v, void* stream) {
 extern "C" int hx_dot(const double* a, const double* b, int64_t lo, int64_t hi, double* work, double* out,
                       void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(a)) return st;
   if (!a || !b || !work || !out) return fail(HX_ERR_INVALID, "null pointer");
   if (lo < 0 || hi < lo) return fail(HX_ERR_INVALID, "bad range");
   return cuda_status(hx_dot_impl(a, b, lo, hi, work, out, static_cast<cudaStream_t>(stream)), "hx_dot");
@@ -325,12 +358,14 @@ extern "C" int hx_dot(const double* a, const double* b, int64_t lo, int64_t hi, 
 extern "C" int hx_cg_update_xr(const double* scal, double* x, const double* p, double* r, const double* ap,
                                int64_t n, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(x)) return st;
   if (!scal || !x || !p || !r || !ap || n < 0) return fail(HX_ERR_INVALID, "bad arguments");
   return cuda_status(hx_cg_xr_impl(scal, x, p, r, ap, n, static_cast<cudaStream_t>(stream)), "hx_cg_update_xr");
 }
 
 extern "C" int hx_cg_update_p(const double* scal, double* p, const double* r, int64_t n, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(p)) return st;
   if (!scal || !p || !r || n < 0) return fail(HX_ERR_INVALID, "bad arguments");
   return cuda_status(hx_cg_p_impl(scal, p, r, n, static_cast<cudaStream_t>(stream)), "hx_cg_update_p");
 }
@@ -338,6 +373,7 @@ extern "C" int hx_cg_update_p(const double* scal, double* p, const double* r, in
 extern "C" int hx_bp5_scatter_dot(const hx_box* box, const double* yl, double* v, const double* p, int64_t n_owned,
                                   double* work, double* out, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(yl)) return st;
   if (int st = box_ok(box)) return st;
   if (!yl || !v || !p || !work || !out) return fail(HX_ERR_INVALID, "null pointer");
   return cuda_status(hx_bp5_scatter_dot_impl(*box, yl, v, p, n_owned, work, out, static_cast<cudaStream_t>(stream)),
@@ -347,6 +383,7 @@ extern "C" int hx_bp5_scatter_dot(const hx_box* box, const double* yl, double* v
 extern "C" int hx_cg_update_xr_dot(const double* scal, double* x, const double* p, double* r, const double* ap,
                                    int64_t n, int64_t n_owned, double* work, double* out, void* stream) {
   g_last_error.clear();
+  if (int st = bind_device(x)) return st;
   if (!scal || !x || !p || !r || !ap || !work || !out || n < 0 || n_owned > n) return fail(HX_ERR_INVALID, "bad arguments");
   return cuda_status(hx_cg_xr_dot_impl(scal, x, p, r, ap, n, n_owned, work, out, static_cast<cudaStream_t>(stream)),
                      "hx_cg_update_xr_dot");

@@ -10,7 +10,8 @@ C2: box_mesh(32, 32, 32, 7, perturbation=0.1, seed=0) -- 32768 trilinear
     elements -- every factor source.
 x = default_rng(0).standard_normal((E, 512, 1)) as in cli.py:194-197.  GPU:
 CUDA events over 200 (C1) / 50 (C2) back-to-back applies after warm-up, inputs
-resident (C2's x+y = 256 MB > L2; C1 fits in L2 and is launch-bound).  CPU:
+resident (C2's x+y = 256 MB > L2; C1 fits in L2 and its API calls are host-bound,
+so C1 is also timed as CUDA-graph replays of the same launch).  CPU:
 best of 3 applies of the oracle with os.cpu_count() threads.
 """
 
@@ -46,6 +47,29 @@ def gpu_time(op, x, y, reps):
     return s.elapsed_time(t) / reps * 1e-3
 
 
+def graph_time(op, x, y, reps):
+    """Device time per apply with the launch captured in a CUDA graph (replayed
+    back to back): what the GPU needs once host launch overhead is out of the way."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        op.apply_(x, y)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(20):
+            op.apply_(x, y)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(max(1, reps // 20)):
+        g.replay()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) * 1e-3 / (20 * max(1, reps // 20))
+
+
 def cpu_time(source, equation, verts, x, kw):
     threads = os.cpu_count() or 1
     st = O.setup(source, equation, ORDER, verts, kw.get("lam0"), kw.get("lam1"))
@@ -68,6 +92,7 @@ def run(config, verts, variants, reps, dev, rows):
         spec = hx.KernelSpec(equation, 1, source, ORDER)
         op = hx.LocalOperator(spec, torch.as_tensor(verts, device=dev), basis, device=dev, **kw)
         t_gpu = gpu_time(op, xd, yd, reps)
+        t_graph = graph_time(op, xd, yd, reps) if E <= 4096 else t_gpu
         got = yd.cpu().numpy()
         t_cpu, threads = cpu_time(source, equation, verts, x, kw)
         want = O.apply_setup(O.setup(source, equation, ORDER, verts, kw.get("lam0"), kw.get("lam1")), x)
@@ -75,9 +100,13 @@ def run(config, verts, variants, reps, dev, rows):
         t_model = max((wc.f_ax + wc.f_geo) / FP64, wc.m_bytes / HBM) * E
         row = dict(config=config, source=source, equation=equation, elements=E,
                    gpu_us=t_gpu * 1e6, gpu_gdofs=E * N3 / t_gpu / 1e9, roofline_frac=t_model / t_gpu,
+                   graph_us=t_graph * 1e6, graph_gdofs=E * N3 / t_graph / 1e9,
                    cpu_ms=t_cpu * 1e3, cpu_gdofs=E * N3 / t_cpu / 1e9, cpu_threads=threads,
                    speedup=t_cpu / t_gpu, rel_diff=O.rel_diff(got, want))
         rows.append(row)
+        if t_graph != t_gpu:
+            print(f"{config} {source:17s} {equation:9s} E={E:6d}  CUDA graph {row['graph_us']:7.2f} us/apply "
+                  f"{row['graph_gdofs']:7.1f} GDOF/s (API calls are host-bound at this size)", flush=True)
         print(f"{config} {source:17s} {equation:9s} E={E:6d}  GPU {row['gpu_us']:9.1f} us {row['gpu_gdofs']:7.1f} GDOF/s "
               f"({100 * row['roofline_frac']:5.1f}% roofline)  CPU[{threads}t] {row['cpu_ms']:9.1f} ms "
               f"{row['cpu_gdofs']:.4f} GDOF/s  x{row['speedup']:8.0f}  rel_diff {row['rel_diff']:.1e}", flush=True)
