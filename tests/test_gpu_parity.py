@@ -311,3 +311,25 @@ def test_apply_inplace_validates_buffers():
             op.apply_(bad, y)
         with pytest.raises(ValueError):
             op.apply_(x, bad)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3, 5, 6, 8, 9, 12, 15])
+def test_every_family_is_deterministic(order):
+    """Shared-memory races show up as run-to-run differences: every kernel family,
+    n_col 1 and 3, three applies each, bitwise equal (and all families agree to 1e-12)."""
+    mesh = _random_box(order, 5, 3, 2, pert=0.15, seed=order)
+    n3 = (order + 1) ** 3
+    kernels = (0, 1, 2, 3) if order <= 2 else (0, 1, 2)
+    for eq, src, ncol in (("poisson", "trilinear", 1), ("helmholtz", "stored", 3), ("poisson", "trilinear-partial", 3)):
+        kw = {"lam0": 1.1, "lam1": 0.7} if eq == "helmholtz" else {}
+        x = torch.randn((mesh.n_elements, n3, ncol), dtype=torch.float64, device=DEV)
+        ref = None
+        for kernel in kernels:
+            op = hx.LocalOperator(hx.KernelSpec(eq, ncol, src, order), mesh, hx.SpectralBasis.build(order), **kw)
+            op.kernel = kernel
+            ys = [op.apply(x) for _ in range(3)]
+            assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2]), (eq, src, ncol, kernel)
+            if ref is None:
+                ref = ys[0]
+            else:
+                assert O.rel_diff(ys[0].cpu().numpy(), ref.cpu().numpy()) <= TOL, (eq, src, ncol, kernel)
