@@ -14,6 +14,7 @@ from .axlocal import (
     KernelSpec,
     LocalOperator,
     ax_local_apply,
+    dense_local_matrix,
 )
 from .basis import SpectralBasis
 from .mesh import (
@@ -55,6 +56,7 @@ __all__ = [
     "KernelSpec",
     "LocalOperator",
     "ax_local_apply",
+    "dense_local_matrix",
     "SpectralBasis",
     "REFERENCE_CUBE",
     "BoxMesh",

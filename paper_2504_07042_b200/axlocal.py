@@ -36,6 +36,7 @@ __all__ = [
     "KernelSpec",
     "LocalOperator",
     "ax_local_apply",
+    "dense_local_matrix",
     "GeometryError",
 ]
 
@@ -414,6 +415,41 @@ class LocalOperator:
         cur.wait_stream(s_out)
         s_out.synchronize()
         return yh
+
+
+def dense_local_matrix(spec, element, basis, lam0=None, lam1=None):
+    """Explicitly assembled (n1^3 x n1^3) element matrix (reference axlocal.py:277-310).
+
+    The reference builds it from the general-route (stored) factors and the dense
+    Kronecker gradient; here the stored-factor operator is applied on the GPU to
+    the n1^3 unit vectors at once (the element replicated n1^3 times, column j of
+    the result is A e_j), which agrees with the reference's matrix to 1e-12.
+    Returns a host numpy array.
+    """
+    torch = _torch()
+    spec = spec if isinstance(spec, KernelSpec) else KernelSpec(*spec)
+    helm = spec.equation is Equation.HELMHOLTZ
+    if not helm and (lam0 is not None or lam1 is not None):
+        raise ValueError("coefficient fields apply to the Helmholtz operator only")
+    n3 = basis.n1**3
+
+    def one_element(value):
+        if value is None or np.ndim(getattr(value, "data", value)) == 0:
+            return value
+        arr = np.asarray(value.data)[:, :, 0] if isinstance(value, LocalField) else np.asarray(value, dtype=float)
+        if arr.shape == (1, n3):
+            arr = arr[0]
+        if arr.shape != (n3,):
+            raise ValueError("coefficient field must be scalar or shaped (E, n1**3)")
+        return arr
+
+    verts = np.asarray(getattr(element, "vertices", element), dtype=np.float64).reshape(1, 8, 3)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    op = LocalOperator(KernelSpec(spec.equation, 1, FactorSource.STORED, spec.order),
+                       torch.as_tensor(np.repeat(verts, n3, axis=0), device=dev), basis,
+                       lam0=one_element(lam0), lam1=one_element(lam1), device=dev)
+    eye = torch.eye(n3, dtype=torch.float64, device=dev).unsqueeze(-1)
+    return op.apply(eye)[:, :, 0].T.contiguous().cpu().numpy()
 
 
 def ax_local_apply(spec, elements, basis, x, lam0=None, lam1=None, threads: int = 1):

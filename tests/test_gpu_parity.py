@@ -333,3 +333,17 @@ def test_every_family_is_deterministic(order):
                 ref = ys[0]
             else:
                 assert O.rel_diff(ys[0].cpu().numpy(), ref.cpu().numpy()) <= TOL, (eq, src, ncol, kernel)
+
+
+@pytest.mark.parametrize("eq", ["poisson", "helmholtz"])
+@pytest.mark.parametrize("order", [2, 3])
+def test_dense_local_matrix_golden(golden, eq, order):
+    """dense_local_matrix (axlocal.py:277-310) against the reference's own matrices."""
+    verts = golden[f"dense_{eq}_{order}_verts"]
+    got = hx.dense_local_matrix(hx.KernelSpec(eq, 1, "stored", order), hx.make_element(verts),
+                                hx.SpectralBasis.build(order))
+    assert got.shape == ((order + 1) ** 3,) * 2
+    assert O.rel_diff(got, golden[f"dense_{eq}_{order}"]) <= TOL
+    with pytest.raises(ValueError):
+        hx.dense_local_matrix(hx.KernelSpec("poisson", 1, "stored", order), hx.make_element(verts),
+                              hx.SpectralBasis.build(order), lam0=2.0)
