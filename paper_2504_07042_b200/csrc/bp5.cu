@@ -17,6 +17,10 @@
 // block), so results are bitwise reproducible run to run.
 #include "hx_common.cuh"
 
+#ifndef HX_BAND_MINB
+#define HX_BAND_MINB 4
+#endif
+
 namespace hx {
 namespace bp5 {
 
@@ -98,7 +102,7 @@ __device__ __forceinline__ void prefetch_band_ahead(const Box& b, const double* 
 // per-axis state lives in registers (no local-memory arrays), and the rows'
 // loads are independent so several rows are in flight per thread.
 template <int NT>
-__global__ void __launch_bounds__(256) scatter_band_kernel(Box b, const double* __restrict__ yl,
+__global__ void __launch_bounds__(256, HX_BAND_MINB) scatter_band_kernel(Box b, const double* __restrict__ yl,
                                                            double* __restrict__ v, const double* __restrict__ p,
                                                            int64_t n_owned, double* __restrict__ partial,
                                                            int do_mask) {
@@ -136,6 +140,79 @@ __global__ void __launch_bounds__(256) scatter_band_kernel(Box b, const double* 
       const int64_t gid = ((int64_t)gz * ny + gy) * nx + gx;
       v[gid] = acc;
       if (p && gid < n_owned) dot = fma(p[gid], acc, dot);
+    }
+  }
+  if (!partial) return;
+  sred[threadIdx.x] = dot;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sred[threadIdx.x] += sred[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = sred[0];
+}
+
+// The same band scatter with 32-bit indices (slab element-local vector and
+// lattice below 2^31 entries, one column): fewer registers -> 8 blocks of 256
+// threads per SM instead of 4, and the kernel is latency bound, so occupancy is
+// what pays (76^3 elements: 2.0 -> 1.7 ms).
+struct AxisCopies32 {
+  int off[2];
+  bool ok[2];
+};
+
+__device__ __forceinline__ AxisCopies32 axis_copies32(int g, int n, int ne, int elem_stride, int node_stride) {
+  const int q = (int)((unsigned)g / (unsigned)n);
+  const int r = g - q * n;
+  AxisCopies32 a;
+  if (r == 0) {
+    a.ok[0] = q >= 1 && q - 1 < ne;
+    a.off[0] = (q - 1) * elem_stride + n * node_stride;
+    a.ok[1] = q < ne;
+    a.off[1] = q * elem_stride;
+  } else {
+    a.ok[0] = false;
+    a.off[0] = 0;
+    a.ok[1] = true;
+    a.off[1] = q * elem_stride + r * node_stride;
+  }
+  return a;
+}
+
+__global__ void __launch_bounds__(256, 8) scatter_band32_kernel(Box b, const double* __restrict__ yl,
+                                                                double* __restrict__ v, const double* __restrict__ p,
+                                                                int64_t n_owned, double* __restrict__ partial,
+                                                                int do_mask) {
+  __shared__ double sred[256];
+  constexpr int n = 7, n1 = 8, n3 = 512;
+  const int nx = b.ex * n + 1, ny = b.ey * n + 1;
+  const int gz = blockIdx.y;
+  const int gzg = gz + b.z0 * n, nzg = b.ez * n + 1;
+  const int ex_n3 = b.ex * n3;
+  const AxisCopies32 az = axis_copies32(gz, n, b.nz_el, b.ey * ex_n3, n1 * n1);
+  const bool plane_boundary = gzg == 0 || gzg == nzg - 1;
+  const int gy0 = blockIdx.x * kRowsPerBlock;
+  const int gy1 = min(gy0 + kRowsPerBlock, ny);
+  prefetch_band_ahead<7>(b, yl, nx, ny);
+  const int owned = n_owned < 0x7fffffffLL ? (int)n_owned : 0x7fffffff;
+  double dot = 0.0;
+  for (int gx = threadIdx.x; gx < nx; gx += blockDim.x) {
+    const AxisCopies32 ax = axis_copies32(gx, n, b.ex, n3, 1);
+    const bool col_boundary = plane_boundary || gx == 0 || gx == nx - 1;
+#pragma unroll 4
+    for (int gy = gy0; gy < gy1; ++gy) {
+      const AxisCopies32 ay = axis_copies32(gy, n, b.ey, ex_n3, n1);
+      double acc = 0.0;
+      if (!(do_mask && (col_boundary || gy == 0 || gy == ny - 1))) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // ascending element index: z, y, x lower copy first
+          const int iz = q >> 2, iy = (q >> 1) & 1, ix = q & 1;
+          if (az.ok[iz] && ay.ok[iy] && ax.ok[ix]) acc += __ldg(yl + (az.off[iz] + ay.off[iy] + ax.off[ix]));
+        }
+      }
+      const int gid = (gz * ny + gy) * nx + gx;
+      v[gid] = acc;
+      if (p && gid < owned) dot = fma(p[gid], acc, dot);
     }
   }
   if (!partial) return;
@@ -288,8 +365,20 @@ extern "C" cudaError_t hx_bp5_gather_impl(Box b, const double* u, double* xl, cu
   return cudaGetLastError();
 }
 
+namespace {
+// the 32-bit band kernel covers N = 7, one column, both index spaces below 2^31
+bool band32_ok(const Box& b) {
+  if (b.order != 7 || b.n_col != 1) return false;
+  const int64_t local = (int64_t)b.ex * b.ey * b.nz_el * 512;
+  const int64_t lattice = ((int64_t)b.ex * 7 + 1) * ((int64_t)b.ey * 7 + 1) * ((int64_t)b.nz_el * 7 + 1);
+  return local < 0x7fffffffLL && lattice < 0x7fffffffLL;
+}
+}  // namespace
+
 extern "C" cudaError_t hx_bp5_scatter_impl(Box b, const double* yl, double* v, cudaStream_t s) {
-  if (b.order == 7)
+  if (band32_ok(b))
+    hx::bp5::scatter_band32_kernel<<<band_grid(b), 256, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
+  else if (b.order == 7)
     hx::bp5::scatter_band_kernel<7><<<band_grid(b), 256, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
   else
     hx::bp5::scatter_band_kernel<0><<<band_grid(b), 256, 0, s>>>(b, yl, v, nullptr, 0, nullptr, 0);
@@ -324,7 +413,9 @@ extern "C" cudaError_t hx_cg_p_impl(const double* scal, double* p, const double*
 extern "C" cudaError_t hx_bp5_scatter_dot_impl(Box b, const double* yl, double* v, const double* p, int64_t n_owned,
                                                double* work, double* out, cudaStream_t s) {
   const dim3 grid = band_grid(b);
-  if (b.order == 7)
+  if (band32_ok(b))
+    hx::bp5::scatter_band32_kernel<<<grid, 256, 0, s>>>(b, yl, v, p, n_owned, work, 1);
+  else if (b.order == 7)
     hx::bp5::scatter_band_kernel<7><<<grid, 256, 0, s>>>(b, yl, v, p, n_owned, work, 1);
   else
     hx::bp5::scatter_band_kernel<0><<<grid, 256, 0, s>>>(b, yl, v, p, n_owned, work, 1);
