@@ -167,6 +167,7 @@ __device__ __forceinline__ void stage_a(int t, const double* __restrict__ v, Tri
 template <bool HELM, bool MERGED, bool PARTIAL>
 struct TriPoly {
   static constexpr bool kTri = true;
+  static constexpr bool kPpd = false;
   static constexpr bool kHelm = HELM;
   double k01[3], k02[2], k12[2], k22, det[3];
   double wji8;
@@ -276,6 +277,7 @@ struct TriPoly {
 template <bool HELM>
 struct StoredN {
   static constexpr bool kTri = false;
+  static constexpr bool kPpd = false;
   static constexpr bool kHelm = HELM;
   const double* g;
   const double* gwj;
@@ -312,6 +314,7 @@ struct StoredN {
 template <bool HELM>
 struct PpdN {
   static constexpr bool kTri = false;
+  static constexpr bool kPpd = true;
   static constexpr bool kHelm = HELM;
   double h[7];
   double wj, wi;
@@ -471,14 +474,16 @@ constexpr int regs_of(int n) { return n <= 12 ? 128 : n <= 13 ? 168 : n <= 15 ? 
 constexpr int kRegs = regs_of(N1);
 #endif
 // trilinear sources at n1 <= 7 run best with 80 registers (96 for Helmholtz, which
-// would spill; more CTAs hide the per-element setup: +5-15 % at N = 3-6), the
-// streaming sources keep 128
+// would spill; more CTAs hide the per-element setup: +5-15 % at N = 3-6), and so
+// does the Poisson parallelepiped kernel at n1 = 10-13; stored keeps the budget
 template <typename F>
 constexpr int regs_for() {
 #ifdef HX_FASTN_REGS
   return kRegs;
 #else
-  return F::kTri && N1 <= 7 ? (F::kHelm ? 96 : 80) : kRegs;
+  if (F::kTri && N1 <= 7) return F::kHelm ? 96 : 80;
+  if (F::kPpd && !F::kHelm && N1 >= 10 && N1 <= 13) return 80;  // +3-21 % at N = 9-12 (stored would lose)
+  return kRegs;
 #endif
 }
 template <typename F>
