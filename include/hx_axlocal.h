@@ -110,6 +110,13 @@ typedef struct {
   int32_t gather;
   int32_t reserved2;
   hx_box gather_box;
+  /* Optional fused CG direction update (BP5, requires gather): when cg_r != NULL the
+   * apply first forms p = r + (cg_scal[2] / cg_scal[0]) * x on the lattice, with
+   * the rounding of the standalone update (solver.py:170), writes it to cg_p_out
+   * (a different lattice vector than x) and applies A to it. */
+  const double* cg_r;
+  const double* cg_scal;
+  double* cg_p_out;
 } hx_axlocal_args;
 
 /* Library version string. */

@@ -80,6 +80,9 @@ class AxArgs(ctypes.Structure):
         ("gather", _i32),
         ("reserved2", _i32),
         ("gather_box", Box),
+        ("cg_r", _c_p),
+        ("cg_scal", _c_p),
+        ("cg_p_out", _c_p),
     ]
 
 

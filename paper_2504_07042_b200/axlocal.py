@@ -322,12 +322,19 @@ class LocalOperator:
         s = _stream(self.device) if stream is None else ctypes.c_void_p(stream)
         _native.check(_native.lib().hx_axlocal(ctypes.byref(args), s))
 
-    def apply_lattice_(self, u, y, box, stream=None):
+    def apply_lattice_(self, u, y, box, stream=None, cg=None):
         """y = A Q u: the element-local x gathered on the fly from the slab lattice
-        vector u of ``box`` (fused BP5 gather; order 7, one column)."""
+        vector u of ``box`` (fused BP5 gather; order 7, one column).  With
+        ``cg = (r, scal, p_out)`` the CG direction update p_out = r + (scal[2] /
+        scal[0]) u is fused in and A is applied to p_out (hx_axlocal_args.cg_r)."""
         args = self._args(u.data_ptr(), y.data_ptr())
         args.gather = 1
         args.gather_box = box
+        if cg is not None:
+            r, scal, p_out = cg
+            args.cg_r = r.data_ptr()
+            args.cg_scal = scal.data_ptr()
+            args.cg_p_out = p_out.data_ptr()
         self._launch(args, stream)
         return y
 

@@ -613,7 +613,8 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
 
 // COPY selects the copy of the D blocks (so two bodies in one kernel do not
 // share constants); XLAND reads x from the single-element TMA landing buffer.
-template <typename F, int NCOL, bool HELM, bool TRI, int COPY = 0, bool XLAND = false, bool VGLOBAL = false>
+template <typename F, int NCOL, bool HELM, bool TRI, int COPY = 0, bool XLAND = false, bool VGLOBAL = false,
+          bool CGP = false>
 __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict__ ap, int64_t e, int b = 0) {
   const hx_axlocal_args& a = *ap;
   double* sX = s_cubeX;
@@ -646,6 +647,18 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       xk[k] = XLAND ? landing_one<NCOL>()[(k * 64 + lin) * NCOL + c] : __ldg(a.x + xoff + k * xstr + c);
+    if constexpr (CGP) {
+      // fused CG direction update on the lattice: p = r + beta p_old (solver.py:170, the
+      // rounding of cg_p_kernel); every element writes its nodes (shared nodes get the
+      // same value from each of their elements)
+      const double beta = a.cg_scal[2] / a.cg_scal[0];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t g = xoff + k * xstr;
+        xk[k] = __dadd_rn(__ldg(a.cg_r + g), __dmul_rn(beta, xk[k]));
+        a.cg_p_out[g] = xk[k];
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) sX[Ak(k) + kp] = xk[k];
     if (TRI && F::kStageA && c == 0) tri_stage_a(t, vsrc, s_tri);
@@ -753,7 +766,7 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
 
 // One CTA per element (no persistent loop): the body inlines into the kernel
 // and D's even-odd blocks stay __constant__ operands.
-template <typename F, int NCOL, bool HELM, bool TRI, int MINB, bool VG = false>
+template <typename F, int NCOL, bool HELM, bool TRI, int MINB, bool VG = false, bool CGP = false>
 __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlocal_args a) {
   const int64_t e = blockIdx.x;
   // CTAs start in blockIdx order, ~148 x 8 resident at a time: warm L2 for the
@@ -769,9 +782,13 @@ __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlo
         const unsigned e32 = (unsigned)ahead, exu = (unsigned)bx.ex, exy = exu * (unsigned)bx.ey;
         const unsigned cz = e32 / exy, rem = e32 - cz * exy, cy = rem / exu, cx = rem - cy * exu;
         const int j = threadIdx.x & 7, k = threadIdx.x >> 3;
-        const double* row = a.x + ((int64_t)(cz * 7 + k) * ny + cy * 7 + j) * nx + cx * 7;
-        prefetch_l2(row);
-        prefetch_l2(row + 7);
+        const int64_t off = ((int64_t)(cz * 7 + k) * ny + cy * 7 + j) * nx + cx * 7;
+        prefetch_l2(a.x + off);
+        prefetch_l2(a.x + off + 7);
+        if (CGP) {
+          prefetch_l2(a.cg_r + off);
+          prefetch_l2(a.cg_r + off + 7);
+        }
       } else if (threadIdx.x == 0) {
         bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
       }
@@ -782,7 +799,7 @@ __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlo
     if (TRI && threadIdx.x < 24) s_verts[0][threadIdx.x] = __ldg(a.verts + e * 24 + threadIdx.x);
     if (TRI) __syncthreads();
   }
-  element_direct<F, NCOL, HELM, TRI, 0, false, VG>(&a, e);
+  element_direct<F, NCOL, HELM, TRI, 0, false, VG, CGP>(&a, e);
 }
 
 // Two elements per CTA in straight-line code: the second element's x and
@@ -1142,6 +1159,10 @@ template <typename F, bool HELM, bool TRI, int MINB, bool VG = false>
 cudaError_t launch_single(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)a.n_elements;
+  if (a.cg_r) {  // fused CG direction update (gather mode, n_col = 1; checked by the caller)
+    ax8s<F, 1, HELM, TRI, MINB, VG, true><<<grid, 64, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   if (a.n_col == 3)
     ax8s<F, 3, HELM, TRI, MINB, VG><<<grid, 64, 0, s>>>(a);
   else

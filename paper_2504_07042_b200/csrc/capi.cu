@@ -218,6 +218,12 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
     if ((int64_t)b.ex * b.ey * b.nz_el != a->n_elements) return fail(HX_ERR_INVALID, "gather box / element mismatch");
     if (a->kernel == 1) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the generic kernel");
   }
+  if (a->cg_r) {
+    if (!a->gather) return fail(HX_ERR_INVALID, "the fused CG update needs the fused lattice gather");
+    if (!a->cg_scal || !a->cg_p_out) return fail(HX_ERR_INVALID, "fused CG update: null scalar / output");
+    if (a->cg_p_out == a->x || a->cg_p_out == a->cg_r)
+      return fail(HX_ERR_INVALID, "fused CG update: p_out must not alias p or r");
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n1 = a->order + 1;
   // kernel 0 at orders 1-2: the element-per-thread kernel wherever it measures fastest

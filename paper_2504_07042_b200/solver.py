@@ -160,12 +160,16 @@ class CudaBackend:
 
     fused_gather = os.environ.get("HX_BP5_FUSED_GATHER", "1") != "0"
 
-    def local_apply_lattice(self, local_op, layout, u, yl):
-        """y = A Q u with the gather fused into the AxLocal loads, when supported."""
-        if not self.fused_gather or local_op.spec.order != 7 or local_op.spec.n_col != 1:
+    def local_apply_lattice(self, local_op, layout, u, yl, cg=None):
+        """y = A Q u with the gather fused into the AxLocal loads, when supported
+        (and, with ``cg = (r, scal, p_out)``, the CG direction update too)."""
+        if not self.supports_lattice_apply(local_op):
             return False
-        local_op.apply_lattice_(u, yl, layout.box())
+        local_op.apply_lattice_(u, yl, layout.box(), cg=cg)
         return True
+
+    def supports_lattice_apply(self, local_op) -> bool:
+        return self.fused_gather and local_op.spec.order == 7 and local_op.spec.n_col == 1
 
 
 # ---------------------------------------------------------------------------
@@ -251,10 +255,13 @@ class GlobalOperator:
     def columns(self, v):
         return [v] if self.spec.n_col == 1 else [v[c] for c in range(self.spec.n_col)]
 
-    def apply(self, u, out=None, dot_with=None, dot_out=None):
+    def apply(self, u, out=None, dot_with=None, dot_out=None, cg_update=None):
         """v = Q^T A Q u on the slab (interfaces completed).  With ``dot_with``
         (single rank, one column) the boundary mask and the dot
-        dot_out = dot_with . v over owned nodes are fused into the scatter."""
+        dot_out = dot_with . v over owned nodes are fused into the scatter.  With
+        ``cg_update = (r, scal, p_new)`` (see :meth:`can_fuse_cg_update`) the CG
+        direction update p_new = r + (scal[2] / scal[0]) u runs inside the AxLocal
+        gather and v = Q^T A Q p_new."""
         torch = _torch()
         L, B = self.layout, self.backend
         nc = self.spec.n_col
@@ -266,7 +273,10 @@ class GlobalOperator:
         fused_gather = nc == 1 and hasattr(B, "local_apply_lattice")
         if fused_gather and timing:
             ev[1].record()
-        if not (fused_gather and B.local_apply_lattice(self.local_op, L, u, self._yl)):
+        if cg_update is not None:
+            if not (fused_gather and B.local_apply_lattice(self.local_op, L, u, self._yl, cg=cg_update)):
+                raise ValueError("the fused CG update needs the fused lattice gather (order 7, one column)")
+        elif not (fused_gather and B.local_apply_lattice(self.local_op, L, u, self._yl)):
             for c, uc in enumerate(self.columns(u)):
                 B.gather(L, uc, self._xl, nc, c)
             if timing:
@@ -289,6 +299,17 @@ class GlobalOperator:
 
     def can_fuse_cg(self) -> bool:
         return self.world.size == 1 and self.spec.n_col == 1 and hasattr(self.backend, "scatter_dot")
+
+    #: fold p = r + beta p into the next apply's lattice gather (HX_BP5_FUSED_P=1).  Off by
+    #: default: at 76^3 it saves 2 % of the trilinear solve, costs 4 % on stored, and the
+    #: AxLocal share of the solve (the reference's reported rate) stops being separable.
+    fuse_p_update = os.environ.get("HX_BP5_FUSED_P", "0") == "1"
+
+    def can_fuse_cg_update(self) -> bool:
+        """p = r + beta p fused into the next apply's lattice gather (N = 7, one rank)."""
+        B = self.backend
+        return (self.fuse_p_update and self.can_fuse_cg() and hasattr(B, "supports_lattice_apply")
+                and B.supports_lattice_apply(self.local_op))
 
     def _exchange_interfaces(self, v):
         """Complete the shared z-planes: both neighbours end with lower + upper."""
@@ -411,8 +432,18 @@ def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mas
     iterations = 0
     fuse = masked and op.can_fuse_cg()
     fuse_update = hasattr(B, "update_xr_dot") and op.spec.n_col == 1
+    # p = r + beta p folded into the next apply's lattice gather (same rounding as the
+    # standalone update, so the iterates are bit-identical); p is double-buffered
+    fuse_p = fuse and op.can_fuse_cg_update()
+    p_next = torch.empty_like(p) if fuse_p else None
+    pending_p = False
     for iterations in range(1, max_iter + 1):
-        if fuse:
+        if fuse_p and pending_p:
+            op.apply(p, out=ap, dot_with=p_next, dot_out=red.scal[1:2], cg_update=(r, red.scal, p_next))
+            p, p_next = p_next, p
+            red.scal[0:1] = red.scal[2:3]  # rr = rr_new, after the update read beta
+            pap = float(red.scal[1].item())
+        elif fuse:
             # ap = M Q^T A Q p and pap = p . ap in one scatter pass
             op.apply(p, out=ap, dot_with=p, dot_out=red.scal[1:2])
             pap = float(red.scal[1].item())
@@ -438,8 +469,11 @@ def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mas
         if rel <= tol:
             converged = True
             break
-        B.update_p(red.scal, p.reshape(-1), r.reshape(-1))  # beta = rr_new / rr
-        red.scal[0:1] = red.scal[2:3]
+        if fuse_p:
+            pending_p = True  # applied by the next iteration's fused gather
+        else:
+            B.update_p(red.scal, p.reshape(-1), r.reshape(-1))  # beta = rr_new / rr
+            red.scal[0:1] = red.scal[2:3]
         rr = rr_new
     return CgReport(iterations, history[-1], history, converged, x)
 

@@ -106,3 +106,17 @@ def test_fused_gather_is_bitwise_the_unfused_path(src):
     finally:
         op.backend.fused_gather = True
     assert torch.equal(fused, plain)
+
+
+def test_fused_p_update_is_bitwise_the_plain_cg():
+    """p = r + beta p folded into the lattice gather: same iterates bit for bit."""
+    mesh = hx.box_mesh(4, 3, 3, 7, perturbation=0.1, seed=5)
+    for src in ("trilinear", "stored"):
+        op = S.GlobalOperator(mesh, hx.KernelSpec("poisson", 1, src, 7), hx.SpectralBasis.build(7))
+        b = torch.randn(op.layout.n_local, dtype=torch.float64, device=DEV)
+        plain = S.cg_solve(op, b, tol=1e-10, max_iter=40)
+        op.fuse_p_update = True
+        assert op.can_fuse_cg_update()
+        fused = S.cg_solve(op, b, tol=1e-10, max_iter=40)
+        assert fused.iterations == plain.iterations and fused.residual_history == plain.residual_history
+        assert torch.equal(fused.solution, plain.solution)
