@@ -32,6 +32,7 @@ from .mesh import (
     make_element,
     parallelepiped_defect,
 )
+from .sharding import ShardedLocalOperator
 from .workload import WorkloadCount, ax_flops, geo_flops, workload_count
 from .roofline import (
     HardwareProfile,
@@ -71,6 +72,7 @@ __all__ = [
     "element_node_coords",
     "make_element",
     "parallelepiped_defect",
+    "ShardedLocalOperator",
     "WorkloadCount",
     "ax_flops",
     "geo_flops",

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import os
 
-__all__ = ["World", "slab_layers", "slab_elements"]
+__all__ = ["World", "slab_layers", "slab_elements", "ShardedLocalOperator"]
 
 
 def slab_layers(ez: int, world_size: int, rank: int) -> tuple[int, int]:
@@ -74,3 +74,108 @@ class World:
     def close(self) -> None:
         if self.pg and self.pg.is_initialized():
             self.pg.destroy_process_group()
+
+
+def _split(E: int, parts: int) -> list:
+    """Contiguous element ranges, as even as possible (lower parts take the remainder)."""
+    base, rem = divmod(E, parts)
+    out, e0 = [], 0
+    for i in range(parts):
+        e1 = e0 + base + (1 if i < rem else 0)
+        out.append((e0, e1))
+        e0 = e1
+    return out
+
+
+class ShardedLocalOperator:
+    """Single-process multi-GPU AxLocal (the ``devices=`` wrapper).
+
+    The element range is split into contiguous chunks, one
+    :class:`~paper_2504_07042_b200.LocalOperator` per device; ``apply`` runs the
+    chunks concurrently (one host thread per device, each with its own stream and
+    H2D / kernel / D2H pipeline) and reassembles the result.  Elements are
+    independent, so the result is bit-identical to one operator over all of them.
+    Same constructor and ``apply`` semantics as ``LocalOperator``; ``elements`` may
+    be Element objects, a BoxMesh / Mesh or an (E, 8, 3) array, coefficient fields
+    scalars, (n1^3,) profiles or (E, n1^3) arrays.
+    """
+
+    def __init__(self, spec, elements, basis, lam0=None, lam1=None, devices=None):
+        import numpy as np
+        import torch
+
+        from .axlocal import LocalOperator
+        from .mesh import BoxMesh, Mesh
+
+        if devices is None:
+            devices = [torch.device("cuda", i) for i in range(torch.cuda.device_count())]
+        self.devices = [torch.device(d) for d in devices]
+        if not self.devices:
+            raise ValueError("no devices to shard over")
+        if isinstance(elements, BoxMesh):
+            items = elements.vertices
+        elif isinstance(elements, Mesh):
+            items = elements.elements
+        elif isinstance(elements, torch.Tensor):
+            items = elements.detach().to("cpu", torch.float64).numpy()
+        elif isinstance(elements, np.ndarray):
+            items = elements
+        else:
+            items = tuple(elements)
+        E = len(items)
+        if E < len(self.devices):
+            raise ValueError(f"{E} elements cannot be shared by {len(self.devices)} devices")
+        self.spec, self.n_elements = spec, E
+        self.ranges = _split(E, len(self.devices))
+        n3 = basis.n1**3
+
+        def part(value, e0, e1):
+            data = getattr(value, "data", value)
+            if value is None or np.ndim(data) == 0 or np.shape(data) == (n3,):
+                return value
+            arr = np.asarray(data)
+            if arr.ndim == 3:  # LocalField-like (E, n3, 1)
+                arr = arr[:, :, 0]
+            if arr.shape != (E, n3):
+                raise ValueError("coefficient field must be scalar or shaped (E, n1**3)")
+            return arr[e0:e1]
+
+        self.parts = [
+            LocalOperator(spec, items[e0:e1], basis, lam0=part(lam0, e0, e1), lam1=part(lam1, e0, e1), device=d)
+            for (e0, e1), d in zip(self.ranges, self.devices)
+        ]
+
+    def apply(self, x, threads: int = 1):
+        """Y = A X: a host LocalField or (E, n1^3[, n_col]) host / CUDA tensor, like
+        LocalOperator.apply; CUDA inputs come back on their own device."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        import numpy as np
+        import torch
+
+        from .mesh import LocalField
+
+        field = isinstance(x, LocalField)
+        if field:
+            if x.n_elements != self.n_elements:
+                raise ValueError("field element count does not match the operator")
+            xt = torch.from_numpy(np.ascontiguousarray(x.data, dtype=np.float64))
+        else:
+            xt = x
+            if xt.shape[0] != self.n_elements:
+                raise ValueError("field element count does not match the operator")
+        out = torch.empty_like(xt)
+
+        def run(i):
+            (e0, e1), op, dev = self.ranges[i], self.parts[i], self.devices[i]
+            with torch.cuda.device(dev):
+                chunk = xt[e0:e1]
+                if chunk.is_cuda and chunk.device != dev:
+                    chunk = chunk.to(dev)
+                y = op.apply(chunk)
+                out[e0:e1].copy_(y)
+                torch.cuda.synchronize(dev)
+
+        with ThreadPoolExecutor(max_workers=len(self.parts)) as pool:
+            list(pool.map(run, range(len(self.parts))))
+        return LocalField(out.numpy(), self.spec.order) if field else out

@@ -347,3 +347,25 @@ def test_dense_local_matrix_golden(golden, eq, order):
     with pytest.raises(ValueError):
         hx.dense_local_matrix(hx.KernelSpec("poisson", 1, "stored", order), hx.make_element(verts),
                               hx.SpectralBasis.build(order), lam0=2.0)
+
+
+def test_sharded_operator_is_bitwise_one_operator():
+    """ShardedLocalOperator (devices= wrapper): chunks on several devices (here the one
+    GPU twice / three times) give the single operator's result bit for bit."""
+    from paper_2504_07042_b200.sharding import ShardedLocalOperator
+
+    order = 5
+    mesh = _random_box(order, 5, 4, 3, pert=0.1, seed=6)
+    n3 = (order + 1) ** 3
+    rng = np.random.default_rng(3)
+    lam0 = rng.uniform(0.5, 2.0, (mesh.n_elements, n3))
+    spec = hx.KernelSpec("helmholtz", 1, "trilinear", order)
+    one = hx.LocalOperator(spec, mesh, hx.SpectralBasis.build(order), lam0=lam0, lam1=0.3)
+    x = rng.standard_normal((mesh.n_elements, n3, 1))
+    want = one.apply(torch.as_tensor(x, device=DEV))
+    for parts in (2, 3):
+        sh = ShardedLocalOperator(spec, mesh, hx.SpectralBasis.build(order), lam0=lam0, lam1=0.3,
+                                  devices=[DEV] * parts)
+        assert torch.equal(sh.apply(torch.as_tensor(x, device=DEV)), want)
+        got = sh.apply(hx.LocalField(x, order))
+        assert np.array_equal(got.data, want.cpu().numpy())
