@@ -233,6 +233,27 @@ def test_c2_config_subset_parity():
         assert O.rel_diff(y[sub], want) <= TOL, src
 
 
+@pytest.mark.parametrize("order,counts", [(7, (128, 128, 96)), (15, (58, 58, 58)), (2, (215, 215, 215))])
+def test_benchmark_scale_subset_parity(order, counts):
+    """At the benchmark scale (C4: 1.57 M elements = 805 M DOF at N=7; ~800 M DOF
+    at N=15 and 2) every large-index path runs: full GPU applies, the oracle on a
+    random 256-element subset."""
+    mesh = hx.box_mesh(*counts, order, perturbation=0.1, seed=0)
+    E, n3 = mesh.n_elements, (order + 1) ** 3
+    rng = np.random.default_rng(order)
+    sub = np.sort(rng.choice(E, 256, replace=False))
+    x = torch.randn((E, n3, 1), dtype=torch.float64, device=DEV)
+    xs = x[torch.as_tensor(sub, device=DEV)].cpu().numpy()
+    verts = mesh.vertices[sub]
+    for src in ("trilinear", "stored"):
+        op = hx.LocalOperator(hx.KernelSpec("poisson", 1, src, order), mesh, hx.SpectralBasis.build(order))
+        y = op.apply(x)
+        got = y[torch.as_tensor(sub, device=DEV)].cpu().numpy()
+        assert O.rel_diff(got, O.apply(src, "poisson", order, verts, xs)) <= TOL, src
+        del op, y
+        torch.cuda.empty_cache()
+
+
 def test_full_size_properties():
     """Size-independent properties at a large size: Poisson annihilates
     constants; the operator is linear and symmetric (u.Av = v.Au per element)."""
