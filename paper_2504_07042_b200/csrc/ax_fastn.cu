@@ -166,10 +166,20 @@ __device__ __forceinline__ void stage_a(int t, const double* __restrict__ v, Tri
 
 template <bool HELM, bool MERGED, bool PARTIAL>
 struct TriPoly {
+  // K00(j,k) / K11(i,k) from shared tables (one entry per thread) or as quadratics in
+  // t per fibre: the tables cost shared bandwidth, the quadratics FP64.  Measured per
+  // order (HX_FASTN_NOTAB builds): quadratics win at n1 = 4, 11, 14 (+3 / +4 / +11 %),
+  // tables elsewhere or within noise.
+#ifdef HX_FASTN_NOTAB
+  static constexpr bool kTab = false;
+#else
+  static constexpr bool kTab = !(N1 == 4 || N1 == 11 || N1 == 14);
+#endif
   static constexpr bool kTri = true;
   static constexpr bool kPpd = false;
   static constexpr bool kHelm = HELM;
   double k01[3], k02[2], k12[2], k22, det[3];
+  double k00[3], k11[3];  // K00 / K11 along the fibre when not tabulated (kTab false)
   double wji8;
   const double* tab00;
   const double* tab11;
@@ -189,7 +199,7 @@ struct TriPoly {
     }
     tab00 = s.t00[fj];
     tab11 = s.t11[fi];
-    {
+    if (kTab) {
       const double tk = s.xs[fi], tj = s.xs[fj];
       double cr[3], cs[3];
 #pragma unroll
@@ -199,6 +209,13 @@ struct TriPoly {
       }
       s.t00[fj][fi] = dot3(cr, cr);
       s.t11[fi][fj] = dot3(cs, cs);
+    } else {
+      k00[0] = dot3(br, br);
+      k00[1] = 2.0 * dot3(br, sr);
+      k00[2] = dot3(sr, sr);
+      k11[0] = dot3(bs, bs);
+      k11[1] = 2.0 * dot3(bs, ss);
+      k11[2] = dot3(ss, ss);
     }
     const double xj = s.xs[fj], xi = s.xs[fi];
     const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
@@ -237,8 +254,8 @@ struct TriPoly {
   __device__ __forceinline__ void node(int n, double x0, double x1, double x2, double& rr, double& ss, double& tt,
                                        double& mass) const {
     const double t = cX<N1>(K);
-    const double a00 = tab00[K];
-    const double a11 = tab11[K];
+    const double a00 = kTab ? tab00[K] : fma(fma(k00[2], t, k00[1]), t, k00[0]);
+    const double a11 = kTab ? tab11[K] : fma(fma(k11[2], t, k11[1]), t, k11[0]);
     const double a01 = fma(fma(k01[2], t, k01[1]), t, k01[0]);
     const double a02 = fma(k02[1], t, k02[0]);
     const double a12 = fma(k12[1], t, k12[0]);
