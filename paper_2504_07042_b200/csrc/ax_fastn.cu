@@ -499,6 +499,7 @@ constexpr int regs_for() {
   return kRegs;
 #else
   if (F::kTri && N1 <= 7) return F::kHelm ? 96 : 80;
+  if (F::kTri && !F::kHelm && N1 == 12) return 96;  // 3 CTAs per SM: +9 % at N = 11
   if (F::kPpd && !F::kHelm && N1 >= 10 && N1 <= 13) return 80;  // +3-21 % at N = 9-12 (stored would lose)
   return kRegs;
 #endif
