@@ -498,9 +498,13 @@ constexpr int regs_for() {
 #ifdef HX_FASTN_REGS
   return kRegs;
 #else
+  // measured per order with tools/build_variant.sh libraries at 80 / 96 / 128 / 168
+  // registers (profiles/r01_register_budgets.txt); Poisson trilinear and parallelepiped:
   if (F::kTri && N1 <= 7) return F::kHelm ? 96 : 80;
-  if (F::kTri && !F::kHelm && N1 == 12) return 96;  // 3 CTAs per SM: +9 % at N = 11
-  if (F::kPpd && !F::kHelm && N1 >= 10 && N1 <= 13) return 80;  // +3-21 % at N = 9-12 (stored would lose)
+  if (F::kTri && !F::kHelm && (N1 == 12 || N1 == 13)) return 96;  // +9 % at N = 11, 12
+  if (F::kPpd && !F::kHelm && (N1 == 7 || (N1 >= 10 && N1 <= 12))) return 80;
+  if (F::kPpd && !F::kHelm && N1 == 13) return 96;
+  if (F::kPpd && !F::kHelm && N1 == 14) return 168;
   return kRegs;
 #endif
 }
