@@ -345,6 +345,24 @@ class LocalOperator:
         self._launch(self._args(x.data_ptr(), y.data_ptr()), stream)
         return y
 
+    def graphed(self, x, y, applies: int = 1):
+        """A CUDA graph of ``applies`` back-to-back ``apply_(x, y)`` launches on these
+        fixed buffers; calling the returned function replays it on the current stream.
+        For small element counts, where a host API call (~14 us) costs more than the
+        kernel (~3 us at E = 512, N = 7; profiles/r01_config_bench_c1_c2.txt)."""
+        torch = _torch()
+        self._check_device_pair(x, y)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.apply_(x, y)  # warm-up outside the capture (basis upload, lazy module load)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(applies):
+                self.apply_(x, y)
+        return graph.replay
+
     def _check_device_pair(self, x, y):
         torch = _torch()
         want = (self.n_elements, self.basis.n1**3, self.spec.n_col)

@@ -390,3 +390,20 @@ def test_sharded_operator_is_bitwise_one_operator():
         assert torch.equal(sh.apply(torch.as_tensor(x, device=DEV)), want)
         got = sh.apply(hx.LocalField(x, order))
         assert np.array_equal(got.data, want.cpu().numpy())
+
+
+def test_graphed_apply_matches_eager():
+    mesh = hx.box_mesh(512, 1, 1, 7)  # C1: 512 small elements, launch-overhead bound
+    op = hx.LocalOperator(hx.KernelSpec("poisson", 1, "parallelepiped", 7), mesh, hx.SpectralBasis.build(7))
+    x = torch.randn((512, 512, 1), dtype=torch.float64, device=DEV)
+    y = torch.empty_like(x)
+    replay = op.graphed(x, y, applies=3)
+    want = op.apply(x)
+    y.zero_()
+    replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+    x.copy_(torch.randn_like(x))  # the graph reads the buffer's current contents
+    replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, op.apply(x))

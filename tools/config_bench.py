@@ -48,26 +48,20 @@ def gpu_time(op, x, y, reps):
 
 
 def graph_time(op, x, y, reps):
-    """Device time per apply with the launch captured in a CUDA graph (replayed
-    back to back): what the GPU needs once host launch overhead is out of the way."""
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        op.apply_(x, y)
-    torch.cuda.current_stream().wait_stream(s)
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        for _ in range(20):
-            op.apply_(x, y)
-    g.replay()
+    """Device time per apply with the launches captured in a CUDA graph
+    (LocalOperator.graphed) and replayed back to back: what the GPU needs once
+    host launch overhead is out of the way."""
+    replay = op.graphed(x, y, applies=20)
+    replay()
     torch.cuda.synchronize()
+    n = max(1, reps // 20)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(max(1, reps // 20)):
-        g.replay()
+    for _ in range(n):
+        replay()
     b.record()
     b.synchronize()
-    return a.elapsed_time(b) * 1e-3 / (20 * max(1, reps // 20))
+    return a.elapsed_time(b) * 1e-3 / (20 * n)
 
 
 def cpu_time(source, equation, verts, x, kw):
