@@ -22,6 +22,7 @@ split is the CUDA grid, and results are bitwise independent of it.
 from __future__ import annotations
 
 import ctypes
+import os
 import enum
 from dataclasses import dataclass
 
@@ -425,7 +426,8 @@ class LocalOperator:
         xd, yd, s_in, s_out = bufs
         cur = torch.cuda.current_stream(dev)
         E = self.n_elements
-        chunk = max(1024, -(-E // 16))
+        # 32 chunks: pipeline fill / drain ~3 % of a step (16: 5.69, 32: 5.82, 64: 5.83 GDOF/s e2e at C4)
+        chunk = max(1024, -(-E // int(os.environ.get("HX_E2E_CHUNKS", "32"))))
         s_in.wait_stream(cur)
         s_out.wait_stream(cur)
         for a in range(0, E, chunk):
