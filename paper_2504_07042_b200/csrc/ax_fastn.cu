@@ -34,8 +34,6 @@ constexpr int EPB = HX_FASTN_EPB;
 #else
 constexpr int EPB = epb_of(N1);
 #endif
-constexpr int NT = T * EPB;                   // threads per CTA
-constexpr int NT_WARPS = (NT + 31) / 32;
 
 constexpr int pj_of(int n) {
   return n == 6 ? 9 : n == 8 ? 9 : n == 10 ? 17 : n == 12 ? 13 : n == 14 ? 17 : n == 16 ? 17 : n;
@@ -389,12 +387,23 @@ struct NodeLoop<END, END> {
                                              double*, double*) {}
 };
 
-// dynamic shared memory: [X | A | B] cubes per element, then TriShared, then vertices
-constexpr size_t kCubesBytes = sizeof(double) * 3 * EPB * CS;
-constexpr size_t kSmemBytes = kCubesBytes + sizeof(TriShared) * EPB + sizeof(double) * 24 * EPB;
+// Packing of elements into a CTA.  The default (EPB, searched cube stride CS) is
+// per order; a source may pack fewer elements (Pack<1 or 2 ...>, unpadded stride).
+template <int EPB_>
+struct Pack {
+  static constexpr int kEpb = EPB_;
+  static constexpr int kThreads = T * EPB_;
+  static constexpr int kWarps = (kThreads + 31) / 32;
+  static constexpr int kStride = EPB_ == EPB ? CS : CUBE;
+  // dynamic shared memory: [X | A | B] cubes per element, then TriShared, then vertices
+  static constexpr size_t kSmem =
+      sizeof(double) * 3 * EPB_ * kStride + sizeof(TriShared) * EPB_ + sizeof(double) * 24 * EPB_;
+};
 
-template <typename F, int NCOL, bool HELM, int MINB>
-__global__ void __launch_bounds__(NT, MINB) axn(const __grid_constant__ hx_axlocal_args a) {
+template <typename F, int NCOL, bool HELM, int MINB, int EPB_>
+__global__ void __launch_bounds__(Pack<EPB_>::kThreads, MINB) axn(const __grid_constant__ hx_axlocal_args a) {
+  constexpr int EPB = EPB_;
+  constexpr int CS = Pack<EPB_>::kStride;
   extern __shared__ __align__(16) double smem[];
   double(*sX)[CS] = reinterpret_cast<double(*)[CS]>(smem);
   double(*sA)[CS] = reinterpret_cast<double(*)[CS]>(smem + EPB * CS);
@@ -508,30 +517,43 @@ constexpr int regs_for() {
   return kRegs;
 #endif
 }
+// elements per CTA: the stored source streams six factor fields per node and prefers
+// smaller CTAs at n1 = 5 and 7 (+3 / +7 %, A/B libraries with -DHX_FASTN_EPB)
+template <typename F>
+constexpr int epb_for() {
+#ifdef HX_FASTN_EPB
+  return EPB;
+#else
+  return (!F::kTri && !F::kPpd) ? (N1 == 5 ? 3 : N1 == 7 ? 2 : EPB) : EPB;
+#endif
+}
+
 template <typename F>
 constexpr int minb_for() {
-  return 65536 / (NT_WARPS * 32 * regs_for<F>()) > 0 ? 65536 / (NT_WARPS * 32 * regs_for<F>()) : 1;
+  constexpr int w = Pack<epb_for<F>()>::kWarps;
+  return 65536 / (w * 32 * regs_for<F>()) > 0 ? 65536 / (w * 32 * regs_for<F>()) : 1;
 }
 
 template <typename F, bool HELM>
 cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
-  const int64_t blocks = (a.n_elements + EPB - 1) / EPB * a.n_col;
+  using P = Pack<epb_for<F>()>;
+  const int64_t blocks = (a.n_elements + P::kEpb - 1) / P::kEpb * a.n_col;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  static_assert(kSmemBytes <= 227 * 1024, "shared memory");
-  auto k1 = axn<F, 1, HELM, minb_for<F>()>;
-  auto k3 = axn<F, 3, HELM, minb_for<F>()>;
+  static_assert(P::kSmem <= 227 * 1024, "shared memory");
+  auto k1 = axn<F, 1, HELM, minb_for<F>(), P::kEpb>;
+  auto k3 = axn<F, 3, HELM, minb_for<F>(), P::kEpb>;
   static bool attr = false;
-  if (!attr && kSmemBytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  if (!attr && P::kSmem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+      e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
     if (e != cudaSuccess) return e;
   }
   attr = true;
   if (a.n_col == 3)
-    k3<<<(unsigned)blocks, NT, kSmemBytes, s>>>(a);
+    k3<<<(unsigned)blocks, P::kThreads, P::kSmem, s>>>(a);
   else
-    k1<<<(unsigned)blocks, NT, kSmemBytes, s>>>(a);
+    k1<<<(unsigned)blocks, P::kThreads, P::kSmem, s>>>(a);
   return cudaGetLastError();
 }
 
