@@ -793,6 +793,14 @@ __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlo
         bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
       }
       if (TRI && threadIdx.x == 0) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
+      // per-node scalar fields of the partial / merged / Helmholtz variants
+      if (threadIdx.x == 1) {
+        if (a.lam_geo) bulk_prefetch_l2(a.lam_geo + ahead * N3, 4096u);
+        if (a.lam2) bulk_prefetch_l2(a.lam2 + ahead * N3, 4096u);
+        if (a.lam3) bulk_prefetch_l2(a.lam3 + ahead * N3, 4096u);
+        if (a.lam0) bulk_prefetch_l2(a.lam0 + ahead * N3, 4096u);
+        if (a.lam1) bulk_prefetch_l2(a.lam1 + ahead * N3, 4096u);
+      }
     }
   }
   if (!VG) {
