@@ -886,6 +886,23 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
   const int rb = Ak(r.rk) + Aj(r.rj);
   const int cb = Ak(r.ck) + r.ci;
   const int lin = r.fj * 8 + r.fi;
+  // warm L2 with the element two waves ahead (as ax8s): its three columns of x, its
+  // vertices and any per-node scalar fields
+  if (a.reserved != 7 && t < 2) {
+    const int64_t ahead = e + 2 * 148 * MINB;
+    if (ahead < a.n_elements) {
+      if (t == 0) {
+        bulk_prefetch_l2(a.x + ahead * N3 * NC, 4096u * NC);
+        if (TRI) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
+      } else {
+        if (a.lam_geo) bulk_prefetch_l2(a.lam_geo + ahead * N3, 4096u);
+        if (a.lam2) bulk_prefetch_l2(a.lam2 + ahead * N3, 4096u);
+        if (a.lam3) bulk_prefetch_l2(a.lam3 + ahead * N3, 4096u);
+        if (a.lam0) bulk_prefetch_l2(a.lam0 + ahead * N3, 4096u);
+        if (a.lam1) bulk_prefetch_l2(a.lam1 + ahead * N3, 4096u);
+      }
+    }
+  }
   // VG: stage A reads the vertices from L1 (no staging barrier)
   const double* vsrc = VG ? a.verts + e * 24 : s_verts[0];
   if (!VG) {
