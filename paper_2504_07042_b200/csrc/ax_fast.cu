@@ -772,7 +772,9 @@ __global__ void __launch_bounds__(64, MINB) ax8s(const __grid_constant__ hx_axlo
   // CTAs start in blockIdx order, ~148 x 8 resident at a time: warm L2 for the
   // element two waves ahead so its CTA's loads do not wait on HBM latency.
   if (a.reserved != 3) {
-    const int64_t ahead = e + kPrefetchAhead;
+    // 1.25 waves of resident CTAs ahead (the stored kernel streams 28 KB per element and
+    // prefers the shorter distance: 109 vs 105 GDOF/s at 2 waves; trilinear is insensitive)
+    const int64_t ahead = e + (a.reserved == 8 ? kPrefetchAhead : 148 * MINB * 5 / 4);
     if (ahead < a.n_elements) {
       if (a.gather) {
         // fused BP5 gather: x is the slab lattice; warm the 64 lattice rows (64 B each)
