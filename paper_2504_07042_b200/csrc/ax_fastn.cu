@@ -7,7 +7,11 @@
 // K11(i,k) in shared tables; factors once per node.  Small elements (n1^2
 // threads) are packed several to a CTA so that warps are (nearly) full.
 // Shared cubes use padded strides (PJ, PK) chosen per order by an offline
-// search over the three access patterns.  n_col = 3 runs each
+// search over the three access patterns (tools/cube_layout_search.py); where
+// tools/role_search.py finds one, a layout whose i-row / j-column tasks are
+// dealt to threads by a table so that every 64-bit shared access is
+// conflict-free (fastn_roles.cuh; any thread may run any element's row or
+// column, they only touch shared memory between barriers).  n_col = 3 runs each
 // column in its own CTA with the factors recomputed (identical per-column
 // arithmetic, so n_col=3 == 3 x n_col=1 bitwise).
 #include "hx_common.cuh"
@@ -15,6 +19,7 @@
 #ifndef HX_N1
 #error "compile with -DHX_N1=<points per direction>"
 #endif
+#include "fastn_roles.cuh"
 
 namespace hx {
 namespace fastn {
@@ -42,15 +47,21 @@ constexpr int pk_of(int n) {
   return n == 2 ? 5 : n == 3 ? 18 : n == 4 ? 19 : n == 6 ? 54 : n == 7 ? 52 : n == 8 ? 72 : n == 10 ? 170
        : n == 12 ? 156 : n == 14 ? 238 : n == 16 ? 272 : n * n;
 }
-constexpr int PJ = pj_of(N1);
-constexpr int PK = pk_of(N1);
-constexpr int CUBE = (N1 - 1) * PK + (N1 - 1) * PJ + N1;
+template <bool R>  // R: the role-table layout (fastn_roles.cuh)
+struct Strides {
+  static constexpr int PJ = R ? kRolePJ : pj_of(N1);
+  static constexpr int PK = R ? kRolePK : pk_of(N1);
+  static constexpr int CUBE = (N1 - 1) * PK + (N1 - 1) * PJ + N1;
+};
 // stride between the cubes of the elements packed in one CTA (tools/cube_layout_search.py:
 // PJ, PK and this stride minimise the weighted shared wavefronts of the three fibre
 // patterns over every warp of the CTA; warps straddle elements when n1^2 is not a
 // multiple of 32)
 constexpr int cs_of(int n) { return n == 2 ? 12 : n == 3 ? 57 : n == 5 ? 137 : n == 6 ? 324 : n == 7 ? 369 : 0; }
-constexpr int CS = cs_of(N1) > CUBE ? cs_of(N1) : CUBE;
+template <bool R>
+constexpr int cs_for() {
+  return cs_of(N1) > Strides<false>::CUBE ? cs_of(N1) : Strides<false>::CUBE;
+}
 
 constexpr int EO = 2 * H * H + 2 * H + 1;  // A[H][H], B[H][H], C[H], R[H], M[mid][mid]
 
@@ -176,6 +187,7 @@ struct TriPoly {
   static constexpr bool kTri = true;
   static constexpr bool kPpd = false;
   static constexpr bool kHelm = HELM;
+  static constexpr bool kMerged = MERGED;
   double k01[3], k02[2], k12[2], k22, det[3];
   double k00[3], k11[3];  // K00 / K11 along the fibre when not tabulated (kTab false)
   double wji8;
@@ -366,7 +378,7 @@ struct PpdN {
 };
 
 // compile-time loop over nodes K = 0..N1-1
-template <int K, int END>
+template <int K, int END, int PK>
 struct NodeLoop {
   template <typename F>
   __device__ __forceinline__ static void run(const F& fac, double* sA, double* sB, int kp, int lin,
@@ -377,33 +389,41 @@ struct NodeLoop {
     sA[adr] = rr;
     sB[adr] = ss;
     yk[K] = mass * xk[K];
-    NodeLoop<K + 1, END>::run(fac, sA, sB, kp, lin, x2, xk, tt, yk);
+    NodeLoop<K + 1, END, PK>::run(fac, sA, sB, kp, lin, x2, xk, tt, yk);
   }
 };
-template <int END>
-struct NodeLoop<END, END> {
+template <int END, int PK>
+struct NodeLoop<END, END, PK> {
   template <typename F>
   __device__ __forceinline__ static void run(const F&, double*, double*, int, int, const double*, const double*,
                                              double*, double*) {}
 };
 
-// Packing of elements into a CTA.  The default (EPB, searched cube stride CS) is
-// per order; a source may pack fewer elements (Pack<1 or 2 ...>, unpadded stride).
-template <int EPB_>
+// Packing of elements into a CTA.  The default (EPB, searched cube stride) is per
+// order; a source may pack fewer elements (Pack<1 or 2 ...>, unpadded stride).
+template <int EPB_, bool R = false>
 struct Pack {
   static constexpr int kEpb = EPB_;
-  static constexpr int kThreads = T * EPB_;
+  // role table (fastn_roles.cuh) for this packing: whole warps, the lanes past the
+  // k-fibre threads take row / column tasks
+  static constexpr bool kRoles = HX_ROLES && R && EPB_ == kRoleEPB;
+  using S = Strides<kRoles>;
+  static constexpr int kFibres = T * EPB_;  // k-fibre threads
+  static constexpr int kThreads = kRoles ? (kFibres + 31) / 32 * 32 : kFibres;
   static constexpr int kWarps = (kThreads + 31) / 32;
-  static constexpr int kStride = EPB_ == EPB ? CS : CUBE;
+  static constexpr int kStride = kRoles ? kRoleCS : EPB_ == EPB ? cs_for<false>() : S::CUBE;
   // dynamic shared memory: [X | A | B] cubes per element, then TriShared, then vertices
   static constexpr size_t kSmem =
       sizeof(double) * 3 * EPB_ * kStride + sizeof(TriShared) * EPB_ + sizeof(double) * 24 * EPB_;
 };
 
+// natural layout: thread (fi, fj) of element le runs its own k-fibre, i-row
+// (j = fi, k = fj) and j-column (i = fi, k = fj)
 template <typename F, int NCOL, bool HELM, int MINB, int EPB_>
-__global__ void __launch_bounds__(Pack<EPB_>::kThreads, MINB) axn(const __grid_constant__ hx_axlocal_args a) {
+__global__ void __launch_bounds__(Pack<EPB_, false>::kThreads, MINB) axn(const __grid_constant__ hx_axlocal_args a) {
   constexpr int EPB = EPB_;
-  constexpr int CS = Pack<EPB_>::kStride;
+  constexpr int CS = Pack<EPB_, false>::kStride;
+  constexpr int PJ = Strides<false>::PJ, PK = Strides<false>::PK;
   extern __shared__ __align__(16) double smem[];
   double(*sX)[CS] = reinterpret_cast<double(*)[CS]>(smem);
   double(*sA)[CS] = reinterpret_cast<double(*)[CS]>(smem + EPB * CS);
@@ -460,7 +480,7 @@ __global__ void __launch_bounds__(Pack<EPB_>::kThreads, MINB) axn(const __grid_c
     __syncthreads();  // also publishes this element's K00/K11 tables
 
     double tt[N1], yk[N1];
-    NodeLoop<0, N1>::run(fac, A, B, kp, lin, x2, xk, tt, yk);
+    NodeLoop<0, N1, PK>::run(fac, A, B, kp, lin, x2, xk, tt, yk);
     double yt[N1];
     eon<1, 0>(tt, yt);
     __syncthreads();
@@ -486,6 +506,130 @@ __global__ void __launch_bounds__(Pack<EPB_>::kThreads, MINB) axn(const __grid_c
         if (HELM) y += yk[k];
         a.y[(e * N3 + k * N1 * N1 + lin) * NCOL + c] = y;
       }
+    }
+  }
+}
+
+// role-table layout (fastn_roles.cuh): whole warps; row / column tasks from the table
+template <typename F, int NCOL, bool HELM, int MINB, int EPB_>
+__global__ void __launch_bounds__(Pack<EPB_, true>::kThreads, MINB) axn_r(const __grid_constant__ hx_axlocal_args a) {
+  using P = Pack<EPB_, true>;
+  static_assert(P::kRoles, "role-table kernel without a table");
+  constexpr int PJ = P::S::PJ, PK = P::S::PK;
+  constexpr int EPB = EPB_;
+  constexpr int CS = P::kStride;
+  extern __shared__ __align__(16) double smem[];
+  double(*sX)[CS] = reinterpret_cast<double(*)[CS]>(smem);
+  double(*sA)[CS] = reinterpret_cast<double(*)[CS]>(smem + EPB * CS);
+  double(*sB)[CS] = reinterpret_cast<double(*)[CS]>(smem + 2 * EPB * CS);
+  TriShared* sT = reinterpret_cast<TriShared*>(smem + 3 * EPB * CS);
+  double(*sV)[24] = reinterpret_cast<double(*)[24]>(reinterpret_cast<char*>(sT) + sizeof(TriShared) * EPB);
+  // k-fibre threads own (element le, fibre t); padding lanes (role tables only) skip
+  // every k-fibre phase and run only their row / column tasks
+  const bool kact = P::kThreads == P::kFibres || (int)threadIdx.x < P::kFibres;
+  const int le = kact ? (int)threadIdx.x / T : EPB - 1, t = kact ? (int)threadIdx.x - le * T : 0;
+  // n_col = 3: the three columns of an element group are three adjacent CTAs (same
+  // arithmetic per column, x / y rows shared through L2); no column loop, whose
+  // loop-invariant constant loads NVVM would hoist into registers
+  const int c = NCOL > 1 ? (int)(blockIdx.x % NCOL) : 0;
+  const int64_t e_raw = (int64_t)(blockIdx.x / NCOL) * EPB + le;
+  const bool valid = kact && e_raw < a.n_elements;
+  const int64_t e = e_raw < a.n_elements ? e_raw : a.n_elements - 1;
+  const int fi = t % N1, fj = t / N1;   // k-fibre (i, j); i-row (j = fi, k = fj); j-column (i = fi, k = fj)
+  const int kp = fj * PJ + fi;
+  const int lin = fj * N1 + fi;
+  double* A = sA[le];
+  double* B = sB[le];
+  double* X = sX[le];
+  // i-row / j-column tasks: with a role table any thread may run the row / column of
+  // any element of the CTA, placed so that every half-warp's 16 bases are distinct
+  // modulo 16 bank pairs (0xffff: no task); else the thread's own (j = fi, k = fj)
+  // row and (i = fi, k = fj) column
+  double* const X0 = sX[0];
+  double* const A0 = sA[0];
+  double* const B0 = sB[0];
+  int rbA = le * CS + fj * PK + fi * PJ, cbA = le * CS + fj * PK + fi;
+#if HX_ROLES
+  if constexpr (P::kRoles) {
+    const unsigned r = __ldg(c_roles + threadIdx.x);
+    rbA = (r & 0xffffu) == 0xffffu ? -1 : (int)(r & 0xffffu);
+    cbA = (r >> 16) == 0xffffu ? -1 : (int)(r >> 16);
+  }
+#endif
+  const bool row_task = !P::kRoles || rbA >= 0;
+  const bool col_task = !P::kRoles || cbA >= 0;
+  if (F::kTri) {
+    if (kact)
+      for (int q = t; q < 24; q += T) sV[le][q] = __ldg(a.verts + e * 24 + q);
+    __syncthreads();
+  }
+
+  double xk[N1];
+  if (kact) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) X[k * PK + kp] = xk[k];
+    if (F::kTri) stage_a(t, sV[le], sT[F::kTri ? le : 0]);
+  }
+  __syncthreads();
+
+  F fac;
+  double x2[N1];
+  if (kact) {
+    fac.prepare(a, e, sT[F::kTri ? le : 0], fi, fj);
+    eon<0, 0>(xk, x2);
+  }
+  {
+    double v[N1], o[N1];
+    if (row_task) {
+#pragma unroll
+      for (int n = 0; n < N1; ++n) v[n] = X0[rbA + n];
+      eon<0, 1>(v, o);
+#pragma unroll
+      for (int n = 0; n < N1; ++n) A0[rbA + n] = o[n];
+    }
+    if (col_task) {
+#pragma unroll
+      for (int n = 0; n < N1; ++n) v[n] = X0[cbA + n * PJ];
+      eon<0, 2>(v, o);
+#pragma unroll
+      for (int n = 0; n < N1; ++n) B0[cbA + n * PJ] = o[n];
+    }
+  }
+  __syncthreads();  // also publishes this element's K00/K11 tables
+
+  double tt[N1], yk[N1], yt[N1];
+  if (kact) {
+    NodeLoop<0, N1, PK>::run(fac, A, B, kp, lin, x2, xk, tt, yk);
+    eon<1, 0>(tt, yt);
+  }
+  __syncthreads();
+  {
+    double v[N1], o[N1];
+    if (row_task) {
+#pragma unroll
+      for (int n = 0; n < N1; ++n) v[n] = A0[rbA + n];
+      eon<1, 1>(v, o);
+#pragma unroll
+      for (int n = 0; n < N1; ++n) A0[rbA + n] = o[n];
+    }
+    if (col_task) {
+#pragma unroll
+      for (int n = 0; n < N1; ++n) v[n] = B0[cbA + n * PJ];
+      eon<1, 2>(v, o);
+#pragma unroll
+      for (int n = 0; n < N1; ++n) B0[cbA + n * PJ] = o[n];
+    }
+  }
+  __syncthreads();
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int adr = k * PK + kp;
+      double y = (A[adr] + B[adr]) + yt[k];
+      if (HELM) y += yk[k];
+      a.y[(e * N3 + k * N1 * N1 + lin) * NCOL + c] = y;
     }
   }
 }
@@ -517,44 +661,71 @@ constexpr int regs_for() {
   return kRegs;
 #endif
 }
+// role-table layout per (source, n_col), measured against the natural layout with
+// A/B libraries (-DHX_NO_ROLES; profiles/r01_roles_ab.txt): Poisson parallelepiped
+// +3-23 % at every order, Poisson trilinear +1-9 % (not n1 = 13, 15: -1 / -9 %);
+// stored (HBM-bound) gains from n1 = 10 for Poisson, only at 16 for Helmholtz;
+// Helmholtz trilinear / parallelepiped gain at n1 = 5, 10, 16 and lose up to 8 %
+// elsewhere, merged everywhere below 16; at n1 = 6 Helmholtz and trilinear
+// n_col = 3 lose 2-8 %; at n1 = 7 the table packs 4 elements (no conflict-free layout
+// for 5) and only Poisson parallelepiped gains
+template <typename F, int NCOL>
+constexpr bool roles_for() {
+  bool r = F::kPpd || N1 >= 10 || N1 == 4;  // Poisson
+  if constexpr (F::kTri) r = !(N1 == 15 || (N1 == 13 && NCOL == 1));
+  if (F::kHelm) r = N1 == 16 || ((F::kTri || F::kPpd) && (N1 == 5 || N1 == 10));
+  if constexpr (F::kTri) r = r && (!F::kMerged || N1 == 16);
+  if (N1 == 6) r = r && (F::kPpd || NCOL == 1);
+  if (N1 == 7) r = r && F::kPpd;
+  return HX_ROLES && r;
+}
+
 // elements per CTA: the stored source streams six factor fields per node and prefers
 // smaller CTAs at n1 = 5 and 7 (+3 / +7 %, A/B libraries with -DHX_FASTN_EPB)
-template <typename F>
+template <typename F, int NCOL>
 constexpr int epb_for() {
 #ifdef HX_FASTN_EPB
   return EPB;
 #else
+  if (roles_for<F, NCOL>()) return kRoleEPB;  // the packing the role table was generated for
   return (!F::kTri && !F::kPpd) ? (N1 == 5 ? 3 : N1 == 7 ? 2 : EPB) : EPB;
 #endif
 }
 
-template <typename F>
+template <typename F, int NCOL>
+using PackFor = Pack<epb_for<F, NCOL>(), roles_for<F, NCOL>()>;
+
+template <typename F, int NCOL>
 constexpr int minb_for() {
-  constexpr int w = Pack<epb_for<F>()>::kWarps;
+  constexpr int w = PackFor<F, NCOL>::kWarps;
   return 65536 / (w * 32 * regs_for<F>()) > 0 ? 65536 / (w * 32 * regs_for<F>()) : 1;
+}
+
+template <typename F, int NCOL, bool HELM>
+cudaError_t launch_ncol(const hx_axlocal_args& a, cudaStream_t s) {
+  using P = PackFor<F, NCOL>;
+  const int64_t blocks = (a.n_elements + P::kEpb - 1) / P::kEpb * NCOL;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  static_assert(P::kSmem <= 227 * 1024, "shared memory");
+  constexpr auto k = [] {
+    if constexpr (roles_for<F, NCOL>())
+      return axn_r<F, NCOL, HELM, minb_for<F, NCOL>(), P::kEpb>;
+    else
+      return axn<F, NCOL, HELM, minb_for<F, NCOL>(), P::kEpb>;
+  }();
+  static bool attr = false;
+  if (!attr && P::kSmem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
+    if (e != cudaSuccess) return e;
+  }
+  attr = true;
+  k<<<(unsigned)blocks, P::kThreads, P::kSmem, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <typename F, bool HELM>
 cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
-  using P = Pack<epb_for<F>()>;
-  const int64_t blocks = (a.n_elements + P::kEpb - 1) / P::kEpb * a.n_col;
-  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  static_assert(P::kSmem <= 227 * 1024, "shared memory");
-  auto k1 = axn<F, 1, HELM, minb_for<F>(), P::kEpb>;
-  auto k3 = axn<F, 3, HELM, minb_for<F>(), P::kEpb>;
-  static bool attr = false;
-  if (!attr && P::kSmem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
-    if (e != cudaSuccess) return e;
-  }
-  attr = true;
-  if (a.n_col == 3)
-    k3<<<(unsigned)blocks, P::kThreads, P::kSmem, s>>>(a);
-  else
-    k1<<<(unsigned)blocks, P::kThreads, P::kSmem, s>>>(a);
-  return cudaGetLastError();
+  return a.n_col == 3 ? launch_ncol<F, 3, HELM>(a, s) : launch_ncol<F, 1, HELM>(a, s);
 }
 
 }  // namespace
