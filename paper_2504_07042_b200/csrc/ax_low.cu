@@ -25,11 +25,71 @@ constexpr int TPB = N1 == 2 ? 128 : 64;  // elements (threads) per block
 // CTAs per SM for the launch bounds (trilinear sources; the others use 7 / 1): n1 = 2
 // caps registers at 128 (70 for the others, 268 vs 211 GDOF/s for ppd at N = 1);
 // n1 = 3 holds 2 x 27 doubles per thread and gets all 255
-constexpr int MINB = N1 == 2 ? 4 : 1;
+#ifndef HX_LOW_MINB  // A/B builds (tools/build_variant.sh)
+#define HX_LOW_MINB (N1 == 2 ? 4 : 1)
+#endif
+constexpr int MINB = HX_LOW_MINB;
 constexpr int PAD = N3 | 1;    // odd stride in doubles: conflict-free 64-bit smem accesses
 
 __host__ __device__ constexpr bool tri_src(int src) {
   return src == HX_TRILINEAR || src == HX_TRILINEAR_MERGED || src == HX_TRILINEAR_PARTIAL;
+}
+
+// Block copies between a block's contiguous global rows (W doubles per element,
+// n_col-strided) and padded shared rows.  Full blocks issue a batch of loads
+// (stores) per thread before the first shared store (global store): the copies are
+// latency bound otherwise (one 8-byte load in flight per thread per iteration);
+// batches of kBatch bound the registers the copy holds next to the element state.
+#ifndef HX_LOW_BATCH
+#define HX_LOW_BATCH 8
+#endif
+constexpr int kBatch = HX_LOW_BATCH;
+template <int W, int P, int STRIDE>
+__device__ __forceinline__ void stage_in(double* __restrict__ s, const double* __restrict__ g, int nb) {
+  if (nb == TPB) {
+#pragma unroll
+    for (int u0 = 0; u0 < W; u0 += kBatch) {
+      double v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (u0 + u < W) v[u] = __ldg(g + (int64_t)((u0 + u) * TPB + threadIdx.x) * STRIDE);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (u0 + u < W) {
+          const int idx = (u0 + u) * TPB + threadIdx.x, l = idx / W, q = idx - l * W;
+          s[l * P + q] = v[u];
+        }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nb * W; idx += TPB) {
+      const int l = idx / W, q = idx - l * W;
+      s[l * P + q] = __ldg(g + (int64_t)idx * STRIDE);
+    }
+  }
+}
+
+template <int W, int P, int STRIDE>
+__device__ __forceinline__ void stage_out(double* __restrict__ g, const double* __restrict__ s, int nb) {
+  if (nb == TPB) {
+#pragma unroll
+    for (int u0 = 0; u0 < W; u0 += kBatch) {
+      double v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (u0 + u < W) {
+          const int idx = (u0 + u) * TPB + threadIdx.x, l = idx / W, q = idx - l * W;
+          v[u] = s[l * P + q];
+        }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (u0 + u < W) g[(int64_t)((u0 + u) * TPB + threadIdx.x) * STRIDE] = v[u];
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nb * W; idx += TPB) {
+      const int l = idx / W, q = idx - l * W;
+      g[(int64_t)idx * STRIDE] = s[l * P + q];
+    }
+  }
 }
 
 template <int NCOL, int SRC, bool HELM>
@@ -46,19 +106,13 @@ __global__ void __launch_bounds__(TPB, tri_src(SRC) ? MINB : (N1 == 2 ? 7 : 1)) 
   const double* vtx = s_vert + threadIdx.x * VP;  // this thread's element, read by each column's pencil
   if constexpr (tri_src(SRC)) {
     // coalesced block copy of the vertices, then each thread keeps its element's 24
-    for (int idx = threadIdx.x; idx < nb * 24; idx += TPB) {
-      const int l = idx / 24, q = idx - l * 24;
-      s_vert[l * VP + q] = __ldg(a.verts + e0 * 24 + idx);
-    }
+    stage_in<24, VP, 1>(s_vert, a.verts + e0 * 24, nb);
     __syncthreads();
   }
 #pragma unroll 1
   for (int c = 0; c < NCOL; ++c) {
     // coalesced block copy of column c: x[(e0 + l) N3 + q] -> s_v[l PAD + q]
-    for (int idx = threadIdx.x; idx < nb * N3; idx += TPB) {
-      const int l = idx / N3, q = idx - l * N3;
-      s_v[l * PAD + q] = __ldg(a.x + ((e0 * N3) + idx) * NCOL + c);
-    }
+    stage_in<N3, PAD, NCOL>(s_v, a.x + e0 * N3 * NCOL + c, nb);
     __syncthreads();
     double x[N3], y[N3];
 #pragma unroll
@@ -108,10 +162,7 @@ __global__ void __launch_bounds__(TPB, tri_src(SRC) ? MINB : (N1 == 2 ? 7 : 1)) 
 #pragma unroll
     for (int q = 0; q < N3; ++q) s_v[threadIdx.x * PAD + q] = y[q];
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nb * N3; idx += TPB) {
-      const int l = idx / N3, q = idx - l * N3;
-      a.y[((e0 * N3) + idx) * NCOL + c] = s_v[l * PAD + q];
-    }
+    stage_out<N3, PAD, NCOL>(a.y + e0 * N3 * NCOL + c, s_v, nb);
     if (NCOL > 1) __syncthreads();
   }
 }
