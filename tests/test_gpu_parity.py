@@ -201,6 +201,37 @@ def test_run_to_run_bitwise(kernel):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("order", [2, 3, 4, 5, 6, 8, 9, 11, 12, 13, 14, 15])
+@pytest.mark.parametrize("dims", [(3, 2, 2), (7, 1, 1), (1, 1, 1)])
+def test_role_table_layouts_every_source(order, dims):
+    """The order-generic kernel's role-table layouts (fastn_roles.cuh: row / column
+    tasks dealt across the elements of a CTA, padding lanes) for every source,
+    equation and n_col, at element counts that leave CTAs partly empty; the
+    default kernel (0) and the fast kernel (2), against the oracle."""
+    mesh = hx.box_mesh(*dims, order, perturbation=0.15, seed=order)
+    shear = np.array([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]])
+    ppd_verts = hx.box_mesh(*dims, order).vertices @ shear.T
+    E, n3 = mesh.n_elements, (order + 1) ** 3
+    rng = np.random.default_rng(order + 100 * dims[0])
+    x = rng.standard_normal((E, n3, 3))
+    lam0 = rng.uniform(0.5, 2.0, (E, n3))
+    lam1 = rng.uniform(0.5, 2.0, (E, n3))
+    cases = [("poisson", s) for s in ("trilinear", "trilinear-partial", "stored", "parallelepiped")]
+    cases += [("helmholtz", s) for s in ("trilinear", "trilinear-merged", "stored", "parallelepiped")]
+    for eq, src in cases:
+        verts = ppd_verts if src == "parallelepiped" else mesh.vertices
+        kw = {"lam0": lam0, "lam1": lam1} if eq == "helmholtz" else {}
+        for n_col in (1, 3):
+            xc = np.ascontiguousarray(x[..., :n_col])
+            want = O.apply(src, eq, order, verts, xc, **kw)
+            for kernel in (0, 2):
+                op = hx.LocalOperator(hx.KernelSpec(eq, n_col, src, order), torch.as_tensor(verts, device=DEV),
+                                      hx.SpectralBasis.build(order), **kw)
+                op.kernel = kernel
+                got = op.apply(torch.as_tensor(xc, device=DEV)).cpu().numpy()
+                assert O.rel_diff(got, want) <= TOL, (order, dims, eq, src, n_col, kernel)
+
+
 @pytest.mark.parametrize("E", [1, 2, 3, 5, 7, 33, 149, 300])
 def test_ragged_element_counts(E):
     """Element counts that do not fill a CTA / wave (tail handling)."""
