@@ -713,12 +713,18 @@ cudaError_t launch_ncol(const hx_axlocal_args& a, cudaStream_t s) {
     else
       return axn<F, NCOL, HELM, minb_for<F, NCOL>(), P::kEpb>;
   }();
-  static bool attr = false;
-  if (!attr && P::kSmem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
+  if (P::kSmem > 48 * 1024) {  // once per device: the attribute lives in each device's module
+    static unsigned long long done = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(done & bit)) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::kSmem);
+      if (e != cudaSuccess) return e;
+      done |= bit;
+    }
   }
-  attr = true;
   k<<<(unsigned)blocks, P::kThreads, P::kSmem, s>>>(a);
   return cudaGetLastError();
 }
