@@ -859,6 +859,18 @@ static __shared__ double s_c3X[3][CUBE];
 static __shared__ double s_c3A[3][CUBE];
 static __shared__ double s_c3B[3][CUBE];
 
+// n_col = 3: keep tt / yt in registers (parallelepiped: +6-12 %) or park them in the
+// x cube (the sources with more per-node state: registers would spill, -5-13 %;
+// A/B in profiles/r01_n7_variants_c4.txt)
+template <typename F>
+struct C3RegTt {
+  static constexpr bool value = false;
+};
+template <bool HELM>
+struct C3RegTt<Ppd<HELM>> {
+  static constexpr bool value = true;
+};
+
 template <typename F>
 __device__ __forceinline__ void apply_factors(const double g[6], double sin, double sout, double x0, double x1,
                                               double x2, double& rr, double& ss, double& tt) {
@@ -945,10 +957,8 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
   }
   __syncthreads();
 
-  // P2: factors once per node, applied to the three columns; tt parked in the
-  // (consumed) x cube at this thread's own fibre positions
-  double mass[8];
-#define HX_NODE3(K)                                                                       \
+  // P2: factors once per node, applied to the three columns
+#define HX_NODE3(K, TT)                                                                   \
   {                                                                                       \
     const int adr = Ak(K) + kp;                                                           \
     double g[6], sin, sout;                                                               \
@@ -958,20 +968,34 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
       apply_factors<F>(g, sin, sout, s_c3A[c][adr], s_c3B[c][adr], x2[c][K], rr, ss, tt); \
       s_c3A[c][adr] = rr;                                                                 \
       s_c3B[c][adr] = ss;                                                                 \
-      s_c3X[c][adr] = tt;                                                                 \
+      TT = tt;                                                                            \
     }                                                                                     \
   }
-  HX_NODE3(0) HX_NODE3(1) HX_NODE3(2) HX_NODE3(3) HX_NODE3(4) HX_NODE3(5) HX_NODE3(6) HX_NODE3(7)
-#undef HX_NODE3
+  double mass[8], yt[NC][8];
+  if constexpr (C3RegTt<F>::value) {
+    // tt in registers (x2[c][K] dies as tt[c][K] is born), then D_t^T tt with the
+    // n_col = 1 kernel's even-odd arithmetic (n_col=3 == 3 x n_col=1 bitwise): saves
+    // the 4 shared accesses per node and column of parking tt / yt in the x cube
+    double tt3[NC][8];
+    HX_NODE3(0, tt3[c][0]) HX_NODE3(1, tt3[c][1]) HX_NODE3(2, tt3[c][2]) HX_NODE3(3, tt3[c][3])
+    HX_NODE3(4, tt3[c][4]) HX_NODE3(5, tt3[c][5]) HX_NODE3(6, tt3[c][6]) HX_NODE3(7, tt3[c][7])
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    double tt[8], yt[8];
+    for (int c = 0; c < NC; ++c) eo8<1>(tt3[c], yt[c]);
+  } else {
+    // tt parked in the (consumed) x cube at this thread's own fibre positions
+    HX_NODE3(0, s_c3X[c][adr]) HX_NODE3(1, s_c3X[c][adr]) HX_NODE3(2, s_c3X[c][adr]) HX_NODE3(3, s_c3X[c][adr])
+    HX_NODE3(4, s_c3X[c][adr]) HX_NODE3(5, s_c3X[c][adr]) HX_NODE3(6, s_c3X[c][adr]) HX_NODE3(7, s_c3X[c][adr])
 #pragma unroll
-    for (int k = 0; k < 8; ++k) tt[k] = s_c3X[c][Ak(k) + kp];
-    eo8<1>(tt, yt);
+    for (int c = 0; c < NC; ++c) {
+      double tt[8], yc[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s_c3X[c][Ak(k) + kp] = yt[k];
+      for (int k = 0; k < 8; ++k) tt[k] = s_c3X[c][Ak(k) + kp];
+      eo8<1>(tt, yc);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_c3X[c][Ak(k) + kp] = yc[k];
+    }
   }
+#undef HX_NODE3
   __syncthreads();
 
   // P3: transposed r and s contractions, in place
@@ -997,7 +1021,7 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
     const int adr = Ak(k) + kp;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      double y = (s_c3A[c][adr] + s_c3B[c][adr]) + s_c3X[c][adr];
+      double y = (s_c3A[c][adr] + s_c3B[c][adr]) + (C3RegTt<F>::value ? yt[c][k] : s_c3X[c][adr]);
       if (HELM) y += mass[k] * __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
       a.y[(e * N3 + k * 64 + lin) * NC + c] = y;
     }
