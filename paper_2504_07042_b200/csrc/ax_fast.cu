@@ -859,15 +859,23 @@ static __shared__ double s_c3X[3][CUBE];
 static __shared__ double s_c3A[3][CUBE];
 static __shared__ double s_c3B[3][CUBE];
 
-// n_col = 3: keep tt / yt in registers (parallelepiped: +6-12 %) or park them in the
-// x cube (the sources with more per-node state: registers would spill, -5-13 %;
+// n_col = 3: keep tt / yt in registers (parallelepiped: +6-12 %; merged at 4 CTAs / SM:
+// +6 %) or park them in the x cube (the other sources: registers would spill, -5-13 %;
 // A/B in profiles/r01_n7_variants_c4.txt)
 template <typename F>
 struct C3RegTt {
+#ifdef HX_C3_REGTT_ALL  // A/B builds
+  static constexpr bool value = true;
+#else
   static constexpr bool value = false;
+#endif
 };
 template <bool HELM>
 struct C3RegTt<Ppd<HELM>> {
+  static constexpr bool value = true;
+};
+template <>  // merged, with 4 CTAs / SM (255 registers): +6 % (launch_c3 below)
+struct C3RegTt<TrilinearPoly<true, true, false, true, false, false, true>> {
   static constexpr bool value = true;
 };
 
@@ -1028,7 +1036,10 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
   }
 }
 
-template <typename F, bool HELM, bool TRI, int MINB = 5>
+#ifndef HX_C3_MINB
+#define HX_C3_MINB 5
+#endif
+template <typename F, bool HELM, bool TRI, int MINB = HX_C3_MINB>
 cudaError_t launch_c3(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements > 0x7fffffffLL) return cudaErrorInvalidValue;
   if (TRI && a.reserved == 6)  // vertices from L1: 7 % slower here (profiles/r01_sweep_variants.txt)
@@ -1257,7 +1268,7 @@ extern "C" cudaError_t hx_fast_launch(const hx_axlocal_args* a, cudaStream_t s) 
       case HX_TRILINEAR_PARTIAL:
         return launch_c3<TrilinearPoly<false, false, true, true, false, false, true>, false, true>(*a, s);
       case HX_TRILINEAR_MERGED:
-        return launch_c3<TrilinearPoly<true, true, false, true, false, false, true>, true, true>(*a, s);
+        return launch_c3<TrilinearPoly<true, true, false, true, false, false, true>, true, true, 4>(*a, s);
       case HX_STORED:
         return helm ? launch_c3<StoredLoad<true>, true, false>(*a, s) : launch_c3<StoredLoad<false>, false, false>(*a, s);
       case HX_PARALLELEPIPED:
