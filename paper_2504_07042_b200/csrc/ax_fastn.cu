@@ -446,15 +446,18 @@ __global__ void __launch_bounds__(Pack<EPB_, false>::kThreads, MINB) axn(const _
   double* X = sX[le];
   double* A = sA[le];
   double* B = sB[le];
-  if (F::kTri) {
-    for (int q = t; q < 24; q += T) sV[le][q] = __ldg(a.verts + e * 24 + q);
-    __syncthreads();
-  }
-
   {
     double xk[N1];
+    if constexpr (F::kTri) {
+      // the fibre's x loads go out before the vertex staging barrier
 #pragma unroll
-    for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
+      for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
+      for (int q = t; q < 24; q += T) sV[le][q] = __ldg(a.verts + e * 24 + q);
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
+    }
 #pragma unroll
     for (int k = 0; k < N1; ++k) X[k * PK + kp] = xk[k];
     if (F::kTri) stage_a(t, sV[le], sT[F::kTri ? le : 0]);
@@ -558,16 +561,20 @@ __global__ void __launch_bounds__(Pack<EPB_, true>::kThreads, MINB) axn_r(const 
 #endif
   const bool row_task = !P::kRoles || rbA >= 0;
   const bool col_task = !P::kRoles || cbA >= 0;
+  // the fibre's x loads go out before the vertex staging barrier (one global latency
+  // per CTA instead of two back to back)
+  double xk[N1];
+  if (kact) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
+  }
   if (F::kTri) {
     if (kact)
       for (int q = t; q < 24; q += T) sV[le][q] = __ldg(a.verts + e * 24 + q);
     __syncthreads();
   }
 
-  double xk[N1];
   if (kact) {
-#pragma unroll
-    for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
 #pragma unroll
     for (int k = 0; k < N1; ++k) X[k * PK + kp] = xk[k];
     if (F::kTri) stage_a(t, sV[le], sT[F::kTri ? le : 0]);
