@@ -925,20 +925,32 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
       }
     }
   }
+  // P0: the three columns of the k-fibre (loads issued before the vertex staging
+  // barrier); x2 = D_t x in registers
+  double x2[NC][8];
+#ifndef HX_C3_XLATE
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x2[c][k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
+#endif
   // VG: stage A reads the vertices from L1 (no staging barrier)
   const double* vsrc = VG ? a.verts + e * 24 : s_verts[0];
   if (!VG) {
     if (TRI && t < 24) s_verts[0][t] = __ldg(a.verts + e * 24 + t);
     if (TRI) __syncthreads();
   }
-
-  // P0: the three columns of the k-fibre; x2 = D_t x in registers
-  double x2[NC][8];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     double xk[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) xk[k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
+    for (int k = 0; k < 8; ++k) {
+#ifndef HX_C3_XLATE
+      xk[k] = x2[c][k];
+#else
+      xk[k] = __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
+#endif
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) s_c3X[c][Ak(k) + kp] = xk[k];
     eo8<0>(xk, x2[c]);
