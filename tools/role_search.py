@@ -83,6 +83,26 @@ def assign(bases, nt):
     return out
 
 
+def assign_greedy(bases, nt):
+    """fallback when no conflict-free dealing exists: tasks (most frequent residue class
+    first) to the half-warp holding the fewest of their class; returns (wavefronts per
+    access instruction summed over half-warps, bases per thread)"""
+    hws = half_warps(nt)
+    nh = len(hws)
+    res = bases % 16
+    cnt = np.zeros((nh, 16), dtype=np.int64)
+    slots = [[] for _ in range(nh)]
+    for q in np.argsort(-np.bincount(res, minlength=16)[res], kind="stable"):
+        h = min((cnt[h, res[q]], len(slots[h]), h) for h in range(nh) if len(slots[h]) < 16)[2]
+        cnt[h, res[q]] += 1
+        slots[h].append(q)
+    out = np.full(nt, -1, dtype=np.int64)
+    for h, (a, b) in enumerate(hws):
+        for i, q in enumerate(slots[h]):
+            out[a + i] = bases[q]
+    return int(cnt.max(axis=1).sum()), out
+
+
 def layout(n1, epb, pj, pk, cs):
     nt = n1 * n1 * epb
     le = np.repeat(np.arange(epb), n1 * n1)
@@ -98,6 +118,8 @@ def padded(n1, epb):
 
 
 def search(n1, epb):
+    """cheapest (PJ, PK, CS): conflict-free if a flow exists, else the fewest wavefronts
+    with greedily dealt rows / columns; ties to the smaller cubes"""
     best = None
     nhk = len(half_warps(n1 * n1 * epb))
     nh = padded(n1, epb) // 16
@@ -109,17 +131,23 @@ def search(n1, epb):
                     continue
                 nt, rows, cols = layout(n1, epb, pj, pk, cs)
                 nt = padded(n1, epb)
-                if max(np.bincount(rows % 16).max(), np.bincount(cols % 16).max()) > nh:
-                    continue
-                r, c = assign(rows, nt), assign(cols, nt)
-                if r is None or c is None:
-                    continue
-                size = 3 * epb * cs
-                if best is None or size < best[0]:
-                    best = (size, pj, pk, cs, r, c)
-        if best is not None:
+                r = c = None
+                if max(np.bincount(rows % 16).max(), np.bincount(cols % 16).max()) <= nh:
+                    r, c = assign(rows, nt), assign(cols, nt)
+                cr, cc = nhk, nhk
+                if r is None:
+                    cr, r = assign_greedy(rows, nt)
+                if c is None:
+                    cc, c = assign_greedy(cols, nt)
+                key = (cr + cc, 3 * epb * cs)
+                if best is None or key < best[0]:
+                    best = (key, pj, pk, cs, r, c)
+        if best is not None and best[0][0] == 2 * nhk:
             break
-    return best
+    if best is None:
+        return None
+    (cost, size), pj, pk, cs, r, c = best
+    return size, pj, pk, cs, r, c, cost - 2 * nhk
 
 
 def main():
@@ -135,8 +163,10 @@ def main():
         if best is None:
             print(f"n1={n1} EPB={epb}: no conflict-free layout in the search range")
             continue
-        size, pj, pk, cs, r, c = best
-        print(f"n1={n1} EPB={epb}: PJ={pj} PK={pk} CS={cs} ({size * 8} B of cubes) conflict-free", flush=True)
+        size, pj, pk, cs, r, c, extra = best
+        print(f"n1={n1} EPB={epb}: PJ={pj} PK={pk} CS={cs} ({size * 8} B of cubes) "
+              + ("conflict-free" if extra == 0 else f"{extra} extra wavefront(s) per row+column access pair"),
+              flush=True)
         assert max(r.max(), c.max()) < 0xffff
         packed = [(int(a) & 0xffff) | ((int(b) & 0xffff) << 16) for a, b in zip(r, c)]  # 0xffff: no task
         if args.emit:
