@@ -670,12 +670,11 @@ constexpr int regs_for() {
 }
 // role-table layout per (source, n_col), measured against the natural layout with
 // A/B libraries (-DHX_NO_ROLES; profiles/r01_roles_ab.txt): Poisson parallelepiped
-// +3-23 % at every order, Poisson trilinear +1-9 % (not n1 = 13, 15: -1 / -9 %);
+// +3-32 % at every order, Poisson trilinear up to +9 % (not n1 = 13, 15: -1 / -9 %);
 // stored (HBM-bound) gains from n1 = 10 for Poisson, only at 16 for Helmholtz;
 // Helmholtz trilinear / parallelepiped gain at n1 = 5, 10, 16 and lose up to 8 %
-// elsewhere, merged everywhere below 16; at n1 = 6 Helmholtz and trilinear
-// n_col = 3 lose 2-8 %; at n1 = 7 the table packs 4 elements (no conflict-free layout
-// for 5) and only Poisson parallelepiped gains
+// elsewhere, merged everywhere below 16; at n1 = 6 Helmholtz and trilinear n_col = 3
+// lose 2-8 %
 template <typename F, int NCOL>
 constexpr bool roles_for() {
   bool r = F::kPpd || N1 >= 10 || N1 == 4;  // Poisson
@@ -683,7 +682,6 @@ constexpr bool roles_for() {
   if (F::kHelm) r = N1 == 16 || ((F::kTri || F::kPpd) && (N1 == 5 || N1 == 10));
   if constexpr (F::kTri) r = r && (!F::kMerged || N1 == 16);
   if (N1 == 6) r = r && (F::kPpd || NCOL == 1);
-  if (N1 == 7) r = r && F::kPpd;
   return HX_ROLES && r;
 }
 

@@ -27,10 +27,11 @@ import numpy as np
 from scipy.sparse import csr_matrix
 from scipy.sparse.csgraph import maximum_flow
 
-# elements per CTA (ax_fastn.cu epb_of; 1 above), except where no conflict-free layout
-# exists for that packing: n1 = 3 packs 10 (90 threads in 3 warps; not 7), n1 = 7 packs
-# 4 (196 threads in 7 warps; not 5)
-EPB = {2: 16, 3: 10, 4: 4, 5: 5, 6: 3, 7: 4}
+# elements per CTA (ax_fastn.cu epb_of; 1 above), except n1 = 3: 10 (90 threads in 3
+# warps) has a conflict-free layout, 7 does not.  n1 = 7 keeps 5 (245 threads, 8 warps)
+# with a greedy dealing (5 extra wavefronts per row + column pair over 16 half-warps),
+# measured better than the conflict-free 4-element packing (196 threads in 7 warps)
+EPB = {2: 16, 3: 10, 4: 4, 5: 5, 6: 3, 7: 5}
 
 
 def half_warps(nt):
