@@ -448,13 +448,18 @@ __global__ void __launch_bounds__(Pack<EPB_, false>::kThreads, MINB) axn(const _
   double* B = sB[le];
   {
     double xk[N1];
-    if constexpr (F::kTri) {
-      // the fibre's x loads go out before the vertex staging barrier
+    if constexpr (F::kTri && N1 <= 11) {
+      // the fibre's x loads go out before the vertex staging barrier (above n1 = 11
+      // the n1 registers held across it cost more than they save: merged -2..-5 %)
 #pragma unroll
       for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
       for (int q = t; q < 24; q += T) sV[le][q] = __ldg(a.verts + e * 24 + q);
       __syncthreads();
     } else {
+      if (F::kTri) {
+        for (int q = t; q < 24; q += T) sV[le][q] = __ldg(a.verts + e * 24 + q);
+        __syncthreads();
+      }
 #pragma unroll
       for (int k = 0; k < N1; ++k) xk[k] = __ldg(a.x + (e * N3 + k * N1 * N1 + lin) * NCOL + c);
     }
@@ -669,17 +674,23 @@ constexpr int regs_for() {
 #endif
 }
 // role-table layout per (source, n_col), measured against the natural layout with
-// A/B libraries (-DHX_NO_ROLES; profiles/r01_roles_ab.txt): Poisson parallelepiped
-// +3-32 % at every order, Poisson trilinear up to +9 % (not n1 = 13, 15: -1 / -9 %);
-// stored (HBM-bound) gains from n1 = 10 for Poisson, only at 16 for Helmholtz;
-// Helmholtz trilinear / parallelepiped gain at n1 = 5, 10, 16 and lose up to 8 %
-// elsewhere, merged everywhere below 16; at n1 = 6 Helmholtz and trilinear n_col = 3
-// lose 2-8 %
+// A/B libraries (profiles/r01_roles_ab.txt): Poisson parallelepiped +3-32 % at every
+// order, Poisson trilinear up to +10 % (not n1 = 13, 15: -1 / -9 %), Poisson stored
+// (HBM-bound) from n1 = 10; Helmholtz per source at the orders where it gained
+// (+2-39 %; elsewhere it lost up to 11 %); merged only at n1 = 16; at n1 = 6
+// trilinear n_col = 3 loses 2-8 %
 template <typename F, int NCOL>
 constexpr bool roles_for() {
   bool r = F::kPpd || N1 >= 10 || N1 == 4;  // Poisson
   if constexpr (F::kTri) r = !(N1 == 15 || (N1 == 13 && NCOL == 1));
-  if (F::kHelm) r = N1 == 16 || ((F::kTri || F::kPpd) && (N1 == 5 || N1 == 10));
+  if (F::kHelm) {
+    if (F::kPpd)
+      r = N1 == 4 || N1 == 5 || N1 == 9 || N1 == 10 || N1 == 16;
+    else if (F::kTri)
+      r = N1 == 5 || N1 == 7 || N1 == 9 || N1 == 10 || N1 == 14 || N1 == 16;
+    else
+      r = N1 == 5 || N1 == 7 || N1 == 9 || N1 == 16;
+  }
   if constexpr (F::kTri) r = r && (!F::kMerged || N1 == 16);
   if (N1 == 6) r = r && (F::kPpd || NCOL == 1);
   return HX_ROLES && r;
