@@ -188,6 +188,7 @@ struct TriPoly {
   static constexpr bool kPpd = false;
   static constexpr bool kHelm = HELM;
   static constexpr bool kMerged = MERGED;
+  static constexpr bool kPartial = PARTIAL;
   double k01[3], k02[2], k12[2], k22, det[3];
   double k00[3], k11[3];  // K00 / K11 along the fibre when not tabulated (kTab false)
   double wji8;
@@ -675,14 +676,15 @@ constexpr int regs_for() {
 }
 // role-table layout per (source, n_col), measured against the natural layout with
 // A/B libraries (profiles/r01_roles_ab.txt): Poisson parallelepiped +3-32 % at every
-// order, Poisson trilinear up to +10 % (not n1 = 13, 15: -1 / -9 %), Poisson stored
+// order, Poisson trilinear up to +10 % (not n1 = 13, 15: -1 / -9 %; partial there
+// +6 / +11 %), Poisson stored
 // (HBM-bound) from n1 = 10; Helmholtz per source at the orders where it gained
 // (+2-39 %; elsewhere it lost up to 11 %); merged only at n1 = 16; at n1 = 6
 // trilinear n_col = 3 loses 2-8 %
 template <typename F, int NCOL>
 constexpr bool roles_for() {
   bool r = F::kPpd || N1 >= 10 || N1 == 4;  // Poisson
-  if constexpr (F::kTri) r = !(N1 == 15 || (N1 == 13 && NCOL == 1));
+  if constexpr (F::kTri) r = F::kPartial || !(N1 == 15 || (N1 == 13 && NCOL == 1));
   if (F::kHelm) {
     if (F::kPpd)
       r = N1 == 4 || N1 == 5 || N1 == 9 || N1 == 10 || N1 == 16;
