@@ -29,6 +29,12 @@ constexpr int TPB = N1 == 2 ? 128 : 64;  // elements (threads) per block
 #define HX_LOW_MINB (N1 == 2 ? 4 : 1)
 #endif
 constexpr int MINB = HX_LOW_MINB;
+// stored / parallelepiped sources: n1 = 2 at 7 CTAs / SM; n1 = 3 parallelepiped at 6
+// for n_col = 1 (168 registers, ~100 B of spills: 250 -> 293 GDOF/s), else 1 (n_col = 3
+// spills at 168: -9 %; stored -14 %)
+constexpr int minb_other(int src, int ncol) {
+  return N1 == 2 ? 7 : (src == HX_PARALLELEPIPED && ncol == 1 ? 6 : 1);
+}
 constexpr int PAD = N3 | 1;    // odd stride in doubles: conflict-free 64-bit smem accesses
 
 __host__ __device__ constexpr bool tri_src(int src) {
@@ -93,7 +99,7 @@ __device__ __forceinline__ void stage_out(double* __restrict__ g, const double* 
 }
 
 template <int NCOL, int SRC, bool HELM>
-__global__ void __launch_bounds__(TPB, tri_src(SRC) ? MINB : (N1 == 2 ? 7 : 1)) ax_low(const hx_axlocal_args a) {
+__global__ void __launch_bounds__(TPB, tri_src(SRC) ? MINB : minb_other(SRC, NCOL)) ax_low(const hx_axlocal_args a) {
   constexpr int VP = 25;  // padded vertex stride (odd: conflict-free)
   __shared__ double s_v[TPB * PAD];                     // x / y of one column
   __shared__ double s_vert[tri_src(SRC) ? TPB * VP : 1];  // the block's vertices (trilinear sources)
