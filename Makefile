@@ -12,7 +12,7 @@ FAST_ORDERS := 2 3 4 5 6 7 9 10 11 12 13 14 15 16
 GEN_OBJS  := $(foreach n,$(ORDERS),$(OBJ)/ax_generic_$(n).o)
 FASTN_OBJS := $(foreach n,$(FAST_ORDERS),$(OBJ)/ax_fastn_$(n).o)
 LOW_OBJS  := $(OBJ)/ax_low_2.o $(OBJ)/ax_low_3.o
-OBJS      := $(GEN_OBJS) $(FASTN_OBJS) $(LOW_OBJS) $(OBJ)/ax_fast.o $(OBJ)/setup.o $(OBJ)/bp5.o $(OBJ)/capi.o
+OBJS      := $(GEN_OBJS) $(FASTN_OBJS) $(LOW_OBJS) $(OBJ)/ax_fast.o $(OBJ)/ax_mma.o $(OBJ)/setup.o $(OBJ)/bp5.o $(OBJ)/capi.o
 HEADERS   := $(SRC)/hx_common.cuh include/hx_axlocal.h $(wildcard $(SRC)/*.cuh)
 
 all: $(LIB)

@@ -57,6 +57,9 @@ cudaError_t hx_upload_basis_fast(int, const double*, const double*, const double
 // specialised kernels (ax_fast.cu): returns cudaErrorNotSupported when no
 // specialised kernel covers the request.
 cudaError_t hx_fast_launch(const hx_axlocal_args*, cudaStream_t);
+// DMMA (mma.sync m8n8k4 f64) N = 7 kernel (ax_mma.cu); NotSupported outside its scope.
+cudaError_t hx_mma_launch(const hx_axlocal_args*, cudaStream_t);
+cudaError_t hx_upload_basis_mma(int, const double*, const double*, const double*);
 
 cudaError_t hx_setup_trilinear_impl(int, int64_t, const double*, int, int64_t*, double*, double*, const double*,
                                     double, const double*, double, cudaStream_t);
@@ -120,7 +123,7 @@ const upload_fn kUploads[] = {
     hx_upload_basis_generic_6,  hx_upload_basis_generic_7,  hx_upload_basis_generic_8,  hx_upload_basis_generic_9,
     hx_upload_basis_generic_10, hx_upload_basis_generic_11, hx_upload_basis_generic_12, hx_upload_basis_generic_13,
     hx_upload_basis_generic_14, hx_upload_basis_generic_15, hx_upload_basis_generic_16, hx_upload_basis_setup,
-    hx_upload_basis_fast,
+    hx_upload_basis_fast,     hx_upload_basis_mma,
 };
 
 int fail(int code, const std::string& msg) {
@@ -234,6 +237,12 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
     if (n1 > 3) return fail(HX_ERR_UNSUPPORTED, "kernel 3 (element per thread) covers orders 1 and 2");
     if (a->gather) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the low-order kernel");
     return cuda_status(n1 == 2 ? hx_low_launch_2(a, s) : hx_low_launch_3(a, s), "hx_axlocal(low)");
+  }
+  if (a->kernel == 4) {  // DMMA kernel (N = 7 trilinear Poisson, n_col 1)
+    cudaError_t e = hx_mma_launch(a, s);
+    if (e == cudaErrorNotSupported)
+      return fail(HX_ERR_UNSUPPORTED, "kernel 4 (DMMA) covers order 7 trilinear Poisson, n_col 1, aligned x/y");
+    return cuda_status(e, "hx_axlocal(mma)");
   }
   if (a->kernel != 1) {
     cudaError_t e = hx_fast_launch(a, s);  // specialised N = 7
