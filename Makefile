@@ -1,6 +1,5 @@
 # Builds the in-tree C-ABI library paper_2504_07042_b200/_lib/libhx_axlocal.so
-# for sm_100a, plus the C oracle helpers.  `make -j` compiles the per-order
-# generic kernel objects in parallel.
+# for sm_100a.  `make -j` compiles the per-order kernel objects in parallel.
 NVCC      ?= nvcc
 ARCH      ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   ?= -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $(ARCH)
@@ -28,6 +27,10 @@ $(OBJ)/ax_low_%.o: $(SRC)/ax_low.cu $(HEADERS) | $(OBJ)
 
 $(OBJ)/ax_fastn_%.o: $(SRC)/ax_fastn.cu $(HEADERS) | $(OBJ)
 	$(NVCC) $(NVFLAGS) -DHX_N1=$* -c $< -o $@
+
+# ax_mma: no implicit FMA contraction (bitwise n_col = 3 == 3 x n_col = 1 across instantiations)
+$(OBJ)/ax_mma.o: $(SRC)/ax_mma.cu $(HEADERS) | $(OBJ)
+	$(NVCC) $(NVFLAGS) -fmad=false -c $< -o $@
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HEADERS) | $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@

@@ -292,10 +292,12 @@ struct StoredLoad {
     tt = fma(g2, x0, fma(g4, x1, g5 * x2));
     mass = 0.0;
     if (HELM) {
+      // __dmul_rn: ptxas must not fuse tt * l0 into the next even-odd add (it can
+      // where tt stays in registers, not where it is parked in shared memory)
       const double l0 = lam0 ? __ldg(lam0 + n) : l0v;
-      rr *= l0;
-      ss *= l0;
-      tt *= l0;
+      rr = __dmul_rn(rr, l0);
+      ss = __dmul_rn(ss, l0);
+      tt = __dmul_rn(tt, l0);
       mass = (lam1 ? __ldg(lam1 + n) : l1v) * __ldg(gwj + n);
     }
   }
@@ -347,10 +349,12 @@ struct Ppd {
     tt = fma(h[2], s0, fma(h[4], s1, h[5] * s2));
     mass = 0.0;
     if (HELM) {
+      // __dmul_rn: ptxas must not fuse tt * l0 into the next even-odd add (it can
+      // where tt stays in registers, not where it is parked in shared memory)
       const double l0 = lam0 ? __ldg(lam0 + n) : l0v;
-      rr *= l0;
-      ss *= l0;
-      tt *= l0;
+      rr = __dmul_rn(rr, l0);
+      ss = __dmul_rn(ss, l0);
+      tt = __dmul_rn(tt, l0);
       mass = (lam1 ? __ldg(lam1 + n) : l1v) * (w * h[6]);
     }
   }
@@ -460,7 +464,7 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
     fac.template apply_at<K>(sc[K], sA[adr], sB[adr], x2[K], rr, ss, tt[K]); \
     sA[adr] = rr;                                                           \
     sB[adr] = ss;                                                           \
-    if (HELM) yk[K] = ms[K] * xk[K];                                        \
+    if (HELM) yk[K] = __dmul_rn(ms[K], xk[K]);                              \
   }
       HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
@@ -472,7 +476,7 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
     node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, tt[K], mass); \
     sA[adr] = rr;                                                                   \
     sB[adr] = ss;                                                                   \
-    if (HELM) yk[K] = mass * xk[K];                                                 \
+    if (HELM) yk[K] = __dmul_rn(mass, xk[K]);                                       \
   }
       HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
@@ -502,7 +506,7 @@ __device__ __noinline__ void element(const hx_axlocal_args* __restrict__ ap, int
     for (int k = 0; k < 8; ++k) {
       const int adr = Ak(k) + kp;
       double y = (sA[adr] + sB[adr]) + yt[k];
-      if (HELM) y += yk[k];
+      if (HELM) y = __dadd_rn(y, yk[k]);  // pinned rounding: n_col=3 == 3 x n_col=1 bitwise
       yout[(k * 64 + lin) * NCOL + c] = y;
     }
   }
@@ -597,7 +601,7 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
     fac.template apply_at<K>(sc[K], sA[adr], sB[adr], x2[K], rr, ss, tt[K]); \
     sA[adr] = rr;                                                           \
     sB[adr] = ss;                                                           \
-    if (HELM) yk[K] = ms[K] * xk[K];                                        \
+    if (HELM) yk[K] = __dmul_rn(ms[K], xk[K]);                              \
   }
       HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
@@ -624,7 +628,7 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
     node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, tt[K], mass); \
     sA[adr] = rr;                                                                   \
     sB[adr] = ss;                                                                   \
-    if (HELM) yk[K] = mass * xk[K];                                                 \
+    if (HELM) yk[K] = __dmul_rn(mass, xk[K]);                                       \
   }
       HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE
@@ -654,7 +658,7 @@ __device__ __forceinline__ void element_direct(const hx_axlocal_args* __restrict
     for (int k = 0; k < 8; ++k) {
       const int adr = Ak(k) + kp;
       double y = (sA[adr] + sB[adr]) + yt[k];
-      if (HELM) y += yk[k];
+      if (HELM) y = __dadd_rn(y, yk[k]);  // pinned rounding: n_col=3 == 3 x n_col=1 bitwise
       yout[(k * 64 + lin) * NCOL + c] = y;
     }
   }
@@ -789,9 +793,9 @@ __device__ __forceinline__ void apply_factors(const double g[6], double sin, dou
   ss = fma(g[1], s0, fma(g[3], s1, g[4] * s2));
   tt = fma(g[2], s0, fma(g[4], s1, g[5] * s2));
   if (F::kOut) {
-    rr *= sout;
-    ss *= sout;
-    tt *= sout;
+    rr = __dmul_rn(rr, sout);
+    ss = __dmul_rn(ss, sout);
+    tt = __dmul_rn(tt, sout);
   }
 }
 
@@ -939,7 +943,7 @@ __global__ void __launch_bounds__(64, MINB) ax8c3(const __grid_constant__ hx_axl
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       double y = (s_c3A[c][adr] + s_c3B[c][adr]) + (C3RegTt<F>::value ? yt[c][k] : s_c3X[c][adr]);
-      if (HELM) y += mass[k] * __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c);
+      if (HELM) y = __dadd_rn(y, __dmul_rn(mass[k], __ldg(a.x + (e * N3 + k * 64 + lin) * NC + c)));
       a.y[(e * N3 + k * 64 + lin) * NC + c] = y;
     }
   }
@@ -1019,7 +1023,7 @@ __device__ __noinline__ void warp_node_phase(const hx_axlocal_args* __restrict__
     node_at<F, K>(fac, K * 64 + lin, sA[adr], sB[adr], x2[K], rr, ss, tt[K], mass); \
     sA[adr] = rr;                                                                   \
     sB[adr] = ss;                                                                   \
-    if (HELM) yk[K] = mass * xk[K];                                                 \
+    if (HELM) yk[K] = __dmul_rn(mass, xk[K]);                                       \
   }
   HX_NODE(0) HX_NODE(1) HX_NODE(2) HX_NODE(3) HX_NODE(4) HX_NODE(5) HX_NODE(6) HX_NODE(7)
 #undef HX_NODE

@@ -12,20 +12,34 @@
 //   Xs = D X_k     A = D: constant D[g][q + 4s].  B = X_k rows: x[k][q + 4s][g],
 //                  a reload of the element's x (L1 hit).
 //   node stage     rr, ss, tt at the thread's two nodes of the slice (x2 = Xt
-//                  from registers), exactly the ax8s arithmetic.
+//                  from registers).
 //   Y  = rr D      A = rr: own values (enumeration 2q + s); B = D[2q + s][g].
 //      + D^T ss    A = D[q + 4s][g]; B = ss rows [q + 4s][g] through a 64-double
-//                  warp tile (the one transpose of the scheme); both products
-//                  accumulate in the same fragment.
+//                  warp tile (the one transpose of the scheme); both products,
+//                  and the Helmholtz mass term, accumulate in one fragment.
 // The t direction is thread-local: a thread owns two whole k-fibres and
 // applies D and D^T to them in registers with the even-odd form.
+//
+// Weight folding (sources whose factors are w (x) something: trilinear,
+// parallelepiped): the node stage runs without the GLL weight w_k of the node's
+// k index, and w_k enters at the end, y_k = w_k (D_r^T rr + D_s^T ss)_k +
+// (D_t^T (w .* tt))_k -- an FMA on the DMMA accumulator, and w folded into the
+// columns of the transposed even-odd blocks (c_EOW; w_m = w_{7-m}).  For the
+// trilinear sources the per-fibre det polynomial is divided by 0.125 w_j w_i
+// once, so a node needs 1/det' and no weight products at all.  The dt column of
+// JT is bilinear, c(i,j) = U_j + xi_i V_j, with U/V per j from stage A.
 //
 // Shared traffic per element: 2 x 512 B for the ss transposes plus the
 // per-element geometry tables, against ~60 KB for the three-ownership ax8s.
 // FP64 work: a DMMA.8x8x4 holds the FP64 pipe for 256 FMAs (the same pipe and
-// rate as DFMA on B200, profiles/r01_ubench_fp64.txt), so the r/s contractions
-// cost 64 FMA per fibre instead of the even-odd 48; DESIGN.md §4.1a has the
-// instruction budget and the measured A/B.
+// rate as DFMA on B200), so the r/s contractions cost 64 FMA per fibre instead
+// of the even-odd 48, and DMMA mixed with DFMA costs ~5.6 pipe cycles per DMMA
+// (profiles/r02_ubench_mix.txt); DESIGN.md §4.1a has the budget and the A/B.
+//
+// n_col = 3 runs one warp per (element, column) with the n_col = 1 code, so
+// n_col = 3 == 3 x n_col = 1 bitwise (test_axlocal.py:180-199); the factor reuse
+// across columns of ax8c3 is given up for that (a column loop makes NVVM hoist
+// the constant operands into registers and spill).
 #include "n7_common.cuh"
 
 // D (row-major [i][m]) for the per-lane fragments (lane-dependent indices: a
@@ -38,6 +52,9 @@ namespace mma {
 using fast::N1;
 using fast::N3;
 
+static __constant__ double c_EOW[2][4][4];  // D^T even-odd blocks, column m scaled by w_m
+static __constant__ double c_IW[8];         // 1 / w_m
+
 // D = A B + C, m8n8k4 f64: A [g][q], B [q][g], C/D [g][2q], [g][2q+1].
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b, double c0, double c1) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
@@ -45,189 +62,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b,
       : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
-// Per-warp shared state: stage-A terms, K00(j,k) / K11(i,k) tables, ss tiles.
-struct WarpShared {
-  fast::TriShared tri;  // j/i/d/xs/ws used; its own tables unused here
-  double t00[8][8];     // [k][j]
-  double t11[8][8];     // [k][i]
-  double tile[2][64];   // ss slice [j][i], ping-pong
-};
-
-// Polynomial-in-t geometry of one k-fibre (j = g, i), TrilinearPoly::prepare.
-struct Fibre {
-  double k01[3], k02[2], k12[2], k22, det[3], wji8;
-};
-
-__device__ __forceinline__ void prepare_fibre(const fast::TriShared& s, int jj, int ii, Fibre& f) {
-  double br[3], sr[3], bs[3], ss[3], c[3];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    br[q] = s.j[jj][q];
-    sr[q] = s.j[jj][3 + q];
-    bs[q] = s.i[ii][q];
-    ss[q] = s.i[ii][3 + q];
-  }
-  const double xj = s.xs[jj], xi = s.xs[ii];
-  const double a0j = 1.0 - xj, a1j = 1.0 + xj, a0i = 1.0 - xi, a1i = 1.0 + xi;
-  const double w00 = a0j * a0i, w01 = a0j * a1i, w10 = a1j * a0i, w11 = a1j * a1i;
-#pragma unroll
-  for (int q = 0; q < 3; ++q) c[q] = w00 * s.d[q] + w01 * s.d[3 + q] + w11 * s.d[6 + q] + w10 * s.d[9 + q];
-  using fast::dot3;
-  f.k01[0] = dot3(br, bs);
-  f.k01[1] = dot3(br, ss) + dot3(sr, bs);
-  f.k01[2] = dot3(sr, ss);
-  f.k02[0] = dot3(br, c);
-  f.k02[1] = dot3(sr, c);
-  f.k12[0] = dot3(bs, c);
-  f.k12[1] = dot3(ss, c);
-  f.k22 = dot3(c, c);
-  const double P[3] = {bs[1] * c[2] - bs[2] * c[1], bs[2] * c[0] - bs[0] * c[2], bs[0] * c[1] - bs[1] * c[0]};
-  const double Q[3] = {ss[1] * c[2] - ss[2] * c[1], ss[2] * c[0] - ss[0] * c[2], ss[0] * c[1] - ss[1] * c[0]};
-  f.det[0] = dot3(br, P);
-  f.det[1] = dot3(br, Q) + dot3(sr, P);
-  f.det[2] = dot3(sr, Q);
-  f.wji8 = 0.125 * (s.ws[jj] * s.ws[ii]);
-}
-
-// rr, ss, tt at node (k = K) of a fibre: the TrilinearPoly<TAB> apply_at order.
-template <int K>
-__device__ __forceinline__ void tri_node(const Fibre& f, double a00, double a11, double x0, double x1, double x2,
-                                         double& rr, double& ss, double& tt) {
-  const double t = cX<N1>(K);
-  const double a01 = fma(fma(f.k01[2], t, f.k01[1]), t, f.k01[0]);
-  const double a02 = fma(f.k02[1], t, f.k02[0]);
-  const double a12 = fma(f.k12[1], t, f.k12[0]);
-  const double g0 = fma(a11, f.k22, -a12 * a12);
-  const double g1 = fma(a02, a12, -a01 * f.k22);
-  const double g2 = fma(a01, a12, -a02 * a11);
-  const double g3 = fma(a00, f.k22, -a02 * a02);
-  const double g4 = fma(a01, a02, -a00 * a12);
-  const double g5 = fma(a00, a11, -a01 * a01);
-  const double dt = fma(fma(f.det[2], t, f.det[1]), t, f.det[0]);
-  const double scale = fast::div_fast(cW<N1>(K) * f.wji8, dt);  // 0.125 w / det(JT)
-  const double s0 = scale * x0, s1 = scale * x1, s2 = scale * x2;
-  rr = fma(g0, s0, fma(g1, s1, g2 * s2));
-  ss = fma(g1, s0, fma(g3, s1, g4 * s2));
-  tt = fma(g2, s0, fma(g4, s1, g5 * s2));
-}
-
-#ifndef HX_MMA_AHEAD_WAVES4
-#define HX_MMA_AHEAD_WAVES4 5  // L2 prefetch distance in quarter waves of resident warps
-#endif
-
-template <int WPB, int MINB>
-__global__ void __launch_bounds__(32 * WPB, MINB) ax8m_v1(const __grid_constant__ hx_axlocal_args a) {
-  __shared__ WarpShared s_w[WPB];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t e = (int64_t)blockIdx.x * WPB + w;
-  if (e >= a.n_elements) return;  // no block-wide barrier below
-  const int g = lane >> 2, q = lane & 3;
-  WarpShared& S = s_w[w];
-
-  // warm L2 with the element ~1.25 waves of resident warps ahead
-  if (lane == 0) {
-    const int64_t ahead = e + (int64_t)148 * WPB * MINB * HX_MMA_AHEAD_WAVES4 / 4;
-    if (ahead < a.n_elements) {
-      bulk_prefetch_l2(a.x + ahead * N3, 4096u);
-      bulk_prefetch_l2(a.verts + ahead * 24, 192u);
-    }
-  }
-  // x in the accumulator layout: x[k][g][2q], x[k][g][2q+1] (16-B loads, 512 B per warp and k)
-  const double* xe = a.x + e * N3;
-  double xa[8], xb[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(xe + k * 64 + g * 8 + 2 * q));
-    xa[k] = v.x;
-    xb[k] = v.y;
-  }
-  // fragments of D
-  double Dr[2], Ds[2], Dt[2], Dy[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    Dr[s] = g_D8[g * 8 + 2 * q + s];
-    Ds[s] = g_D8[g * 8 + q + 4 * s];
-    Dt[s] = g_D8[(2 * q + s) * 8 + g];
-    Dy[s] = g_D8[(q + 4 * s) * 8 + g];
-  }
-  // stage A (vertices straight from global / L1), then the K00 / K11 tables
-  const double* vg = a.verts + e * 24;
-  fast::tri_stage_a(lane, vg, S.tri);
-  fast::tri_stage_a(lane + 32, vg, S.tri);
-  __syncwarp();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int kk = 2 * q + h;
-    const double tk = S.tri.xs[kk];
-    double cr[3], cs[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      cr[c] = S.tri.j[g][c] + tk * S.tri.j[g][3 + c];
-      cs[c] = S.tri.i[g][c] + tk * S.tri.i[g][3 + c];
-    }
-    S.t00[kk][g] = fast::dot3(cr, cr);
-    S.t11[kk][g] = fast::dot3(cs, cs);
-  }
-  Fibre f0, f1;
-  prepare_fibre(S.tri, g, 2 * q, f0);
-  prepare_fibre(S.tri, g, 2 * q + 1, f1);
-  __syncwarp();
-
-  // t direction forward, in registers
-  double ta[8], tb[8];
-  fast::eo8<0>(xa, ta);
-  fast::eo8<0>(xb, tb);
-
-#define HX_SLICE(K)                                                                                \
-  {                                                                                                \
-    double r0, r1, s0, s1;                                                                         \
-    dmma(r0, r1, xa[K], Dr[0], 0.0, 0.0);                                                          \
-    dmma(r0, r1, xb[K], Dr[1], r0, r1);                                                            \
-    const double bx0 = __ldg(xe + K * 64 + q * 8 + g), bx1 = __ldg(xe + K * 64 + (q + 4) * 8 + g); \
-    dmma(s0, s1, Ds[0], bx0, 0.0, 0.0);                                                            \
-    dmma(s0, s1, Ds[1], bx1, s0, s1);                                                              \
-    const double a00 = S.t00[K][g];                                                                \
-    const double2 a11 = *reinterpret_cast<const double2*>(&S.t11[K][2 * q]);                       \
-    double rr0, ss0, rr1, ss1;                                                                     \
-    tri_node<K>(f0, a00, a11.x, r0, s0, ta[K], rr0, ss0, ta[K]);                                   \
-    tri_node<K>(f1, a00, a11.y, r1, s1, tb[K], rr1, ss1, tb[K]);                                   \
-    double* tl = S.tile[K & 1];                                                                    \
-    *reinterpret_cast<double2*>(tl + g * 8 + 2 * q) = make_double2(ss0, ss1);                      \
-    __syncwarp();                                                                                  \
-    double y0, y1;                                                                                 \
-    dmma(y0, y1, rr0, Dt[0], 0.0, 0.0);                                                            \
-    dmma(y0, y1, rr1, Dt[1], y0, y1);                                                              \
-    dmma(y0, y1, Dy[0], tl[q * 8 + g], y0, y1);                                                    \
-    dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);                                              \
-    xa[K] = y0;                                                                                    \
-    xb[K] = y1;                                                                                    \
-  }
-  HX_SLICE(0) HX_SLICE(1) HX_SLICE(2) HX_SLICE(3) HX_SLICE(4) HX_SLICE(5) HX_SLICE(6) HX_SLICE(7)
-#undef HX_SLICE
-
-  // t direction transposed, in registers; y = (D_r^T rr + D_s^T ss) + D_t^T tt
-  double ya[8], yb[8];
-  fast::eo8<1>(ta, ya);
-  fast::eo8<1>(tb, yb);
-  double* ye = a.y + e * N3;
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    *reinterpret_cast<double2*>(ye + k * 64 + g * 8 + 2 * q) = make_double2(xa[k] + ya[k], xb[k] + yb[k]);
-}
-
-
-// ---------------------------------------------------------------------------
-// v2: the GLL weights and 0.125 w_j w_i leave the per-node work.
-//  * lam_geo w_k-free: the node stage uses 1 / det'(t) with det' = det / (0.125 w_j w_i)
-//    (the per-fibre det polynomial scaled once), so a node pays no weight products
-//    and the reciprocal needs no numerator;
-//  * w_k enters at the end: y_k = w_k (D_r^T rr' + D_s^T ss')_k + (D_t^T (w .* tt'))_k,
-//    the first term an FMA on the DMMA accumulator, the second with w folded into
-//    the columns of the transposed even-odd blocks (c_EOW; w_m = w_{7-m});
-//  * the dt column c(i,j) = U_j + xi_i V_j (bilinear), U/V per j from stage A.
-static __constant__ double c_EOW[2][4][4];  // D^T even-odd blocks, column m scaled by w_m
-static __constant__ double c_IW[8];         // 1 / w_m
-
+// Per-warp shared state.
 struct ElemGeo {
   double jb[8][6];   // dr_base[3], dr_slope[3] per j (common_terms, geometry.py:135-184)
   double ib[8][6];   // ds_base[3], ds_slope[3] per i
@@ -239,20 +74,22 @@ struct ElemGeo {
   double tile[2][64];
 };
 
-__device__ __forceinline__ void stage_a2(int t, const double* __restrict__ v, ElemGeo& s) {
+// Stage A of the trilinear geometry: 72 short tasks (one coordinate of a j-side
+// or i-side base/slope pair, or of a U/V pair) plus the point / weight copies.
+__device__ __forceinline__ void stage_a(int t, const double* __restrict__ v, ElemGeo& s) {
   if (t < 72) {
     const int side = t / 24, task = t - 24 * side, idx = task / 3, c = task % 3;
     const double xi = fast::xr(idx);
     const double a0 = 1.0 - xi, a1 = 1.0 + xi;
-    // j side: a0 (v1-v0) + a1 (v3-v2) | a0 (v5-v4) + a1 (v7-v6)
+    // j side: a0 (v1-v0) + a1 (v3-v2) | a0 (v5-v4) + a1 (v7-v6)   (geometry.py:152-167)
     // i side: a0 (v2-v0) + a1 (v3-v1) | a0 (v6-v4) + a1 (v7-v5)
-    // dt col: a0 (v4-v0) + a1 (v6-v2) | a0 (v5-v1) + a1 (v7-v3)   (L | R, a = 1 -/+ xj)
+    // dt col: a0 (v4-v0) + a1 (v6-v2) | a0 (v5-v1) + a1 (v7-v3)   (L | R with a = 1 -/+ xj)
     const int p0 = side == 0 ? 1 : side == 1 ? 2 : 4, q0 = 0;
     const int p1 = side == 0 ? 3 : side == 1 ? 3 : 6, q1 = side == 0 ? 2 : side == 1 ? 1 : 2;
     const int p2 = side == 0 ? 5 : side == 1 ? 6 : 5, q2 = side == 2 ? 1 : 4;
     const int p3 = 7, q3 = side == 0 ? 6 : side == 1 ? 5 : 3;
-    const double lo = a0 * (v[p0 * 3 + c] - v[q0 * 3 + c]) + a1 * (v[p1 * 3 + c] - v[q1 * 3 + c]);
-    const double hi = a0 * (v[p2 * 3 + c] - v[q2 * 3 + c]) + a1 * (v[p3 * 3 + c] - v[q3 * 3 + c]);
+    const double lo = fma(a1, v[p1 * 3 + c] - v[q1 * 3 + c], a0 * (v[p0 * 3 + c] - v[q0 * 3 + c]));
+    const double hi = fma(a1, v[p3 * 3 + c] - v[q3 * 3 + c], a0 * (v[p2 * 3 + c] - v[q2 * 3 + c]));
     double* out = side == 0 ? s.jb[idx] : side == 1 ? s.ib[idx] : s.uv[idx];
     out[c] = lo + hi;
     out[3 + c] = hi - lo;
@@ -262,7 +99,7 @@ __device__ __forceinline__ void stage_a2(int t, const double* __restrict__ v, El
   }
 }
 
-// w .* tt, then D^T: the transposed even-odd contraction with c_EOW.
+// w .* v, then D^T: the transposed even-odd contraction with c_EOW.
 __device__ __forceinline__ void eo8w(const double v[8], double out[8]) {
   double ue[4], uo[4];
 #pragma unroll
@@ -284,13 +121,49 @@ __device__ __forceinline__ void eo8w(const double v[8], double out[8]) {
   }
 }
 
-struct Fibre2 {
-  double k01[3], k02[2], k12[2], k22, det[3];  // det' = det(JT) / (0.125 w_j w_i)
+// Lane context handed to the factor policies.
+struct Lane {
+  int g, q;
+  int64_t e;
 };
 
-__device__ __forceinline__ void prepare_fibre2(const ElemGeo& s, const double br[3], const double sr[3],
-                                               const double U[3], const double V[3], double aj, int ii,
-                                               Fibre2& f) {
+__device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+// (rr, ss, tt) = G (s x0, s x1, s x2) with G symmetric, the reference's row order.
+__device__ __forceinline__ void symv(double g0, double g1, double g2, double g3, double g4, double g5, double s,
+                                     double x0, double x1, double x2, double& rr, double& ss, double& tt) {
+  const double s0 = s * x0, s1 = s * x1, s2 = s * x2;
+  rr = fma(g0, s0, fma(g1, s1, g2 * s2));
+  ss = fma(g1, s0, fma(g3, s1, g4 * s2));
+  tt = fma(g2, s0, fma(g4, s1, g5 * s2));
+}
+
+// ---------------------------------------------------------------------------
+// Factor policies (axlocal.py:171-211).  prepare() once per element after
+// stage A; slice<K>() for the thread's two nodes of slice K: inputs the three
+// derivatives (and x for the mass term), outputs rr, ss, tt and the mass term
+// to add to y (all in the weight-folded domain when kWFold).
+
+// Explicit FMAs (and -fmad=false for this unit, Makefile): every kernel built
+// from these templates rounds identically, which the bitwise n_col = 3 ==
+// 3 x n_col = 1 contract needs (contraction choices otherwise vary per instantiation).
+__device__ __forceinline__ double dot3(const double* u, const double* v) {
+  return fma(u[2], v[2], fma(u[1], v[1], u[0] * v[0]));
+}
+__device__ __forceinline__ void cross(const double* u, const double* v, double* w) {
+  w[0] = fma(u[1], v[2], -(u[2] * v[1]));
+  w[1] = fma(u[2], v[0], -(u[0] * v[2]));
+  w[2] = fma(u[0], v[1], -(u[1] * v[0]));
+}
+
+// Polynomial-in-t trilinear geometry of one k-fibre (j = g, i); det' = det / (0.125 w_j w_i).
+struct TriFibre {
+  double k01[3], k02[2], k12[2], k22, det[3];
+};
+
+template <bool DET>
+__device__ __forceinline__ void tri_fibre(const ElemGeo& s, const double br[3], const double sr[3],
+                                          const double U[3], const double V[3], double aj, int ii, TriFibre& f) {
   double bs[3], ss[3], c[3];
   const double xi = s.xs[ii];
 #pragma unroll
@@ -299,7 +172,6 @@ __device__ __forceinline__ void prepare_fibre2(const ElemGeo& s, const double br
     ss[q] = s.ib[ii][3 + q];
     c[q] = fma(xi, V[q], U[q]);
   }
-  using fast::dot3;
   f.k01[0] = dot3(br, bs);
   f.k01[1] = dot3(br, ss) + dot3(sr, bs);
   f.k01[2] = dot3(sr, ss);
@@ -308,76 +180,48 @@ __device__ __forceinline__ void prepare_fibre2(const ElemGeo& s, const double br
   f.k12[0] = dot3(bs, c);
   f.k12[1] = dot3(ss, c);
   f.k22 = dot3(c, c);
-  const double P[3] = {bs[1] * c[2] - bs[2] * c[1], bs[2] * c[0] - bs[0] * c[2], bs[0] * c[1] - bs[1] * c[0]};
-  const double Q[3] = {ss[1] * c[2] - ss[2] * c[1], ss[2] * c[0] - ss[0] * c[2], ss[0] * c[1] - ss[1] * c[0]};
-  const double gam = aj * s.iw[ii];  // 8 / (w_j w_i)
-  f.det[0] = gam * dot3(br, P);
-  f.det[1] = gam * (dot3(br, Q) + dot3(sr, P));
-  f.det[2] = gam * dot3(sr, Q);
+  if (DET) {
+    // det(JT) = (br + t sr) . ((bs + t ss) x c)
+    double P[3], Q[3];
+    cross(bs, c, P);
+    cross(ss, c, Q);
+    const double gam = aj * s.iw[ii];  // 8 / (w_j w_i)
+    f.det[0] = gam * dot3(br, P);
+    f.det[1] = gam * (dot3(br, Q) + dot3(sr, P));
+    f.det[2] = gam * dot3(sr, Q);
+  }
 }
 
-// rr', ss', tt' = (1 / det'(t_K)) adj(K(t_K)) (x0, x1, x2): the weight-free node stage.
+// adj(K(t_K)) (unscaled g of geometry.py:329-339) of a fibre.
 template <int K>
-__device__ __forceinline__ void tri_node2(const Fibre2& f, double a00, double a11, double x0, double x1,
-                                          double x2, double& rr, double& ss, double& tt) {
+__device__ __forceinline__ void tri_adj(const TriFibre& f, double a00, double a11, double g[6]) {
   const double t = cX<N1>(K);
   const double a01 = fma(fma(f.k01[2], t, f.k01[1]), t, f.k01[0]);
   const double a02 = fma(f.k02[1], t, f.k02[0]);
   const double a12 = fma(f.k12[1], t, f.k12[0]);
-  const double g0 = fma(a11, f.k22, -a12 * a12);
-  const double g1 = fma(a02, a12, -a01 * f.k22);
-  const double g2 = fma(a01, a12, -a02 * a11);
-  const double g3 = fma(a00, f.k22, -a02 * a02);
-  const double g4 = fma(a01, a02, -a00 * a12);
-  const double g5 = fma(a00, a11, -a01 * a01);
-  const double dt = fma(fma(f.det[2], t, f.det[1]), t, f.det[0]);
+  g[0] = fma(a11, f.k22, -a12 * a12);
+  g[1] = fma(a02, a12, -a01 * f.k22);
+  g[2] = fma(a01, a12, -a02 * a11);
+  g[3] = fma(a00, f.k22, -a02 * a02);
+  g[4] = fma(a01, a02, -a00 * a12);
+  g[5] = fma(a00, a11, -a01 * a01);
+}
+
+// 1 / det'(t_K): MUFU seed r, e = 1 - d r, r (1 + e + e^2)  (error ~ e^3).
+template <int K>
+__device__ __forceinline__ double tri_rdet(const TriFibre& f, double& dt) {
+  const double t = cX<N1>(K);
+  dt = fma(fma(f.det[2], t, f.det[1]), t, f.det[0]);
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(dt));
   const double e = fma(-dt, r, 1.0);
-  const double lam = fma(fma(e, e, e), r, r);  // 1 / det'   (error ~ e^3)
-  const double s0 = lam * x0, s1 = lam * x1, s2 = lam * x2;
-  rr = fma(g0, s0, fma(g1, s1, g2 * s2));
-  ss = fma(g1, s0, fma(g3, s1, g4 * s2));
-  tt = fma(g2, s0, fma(g4, s1, g5 * s2));
+  return fma(fma(e, e, e), r, r);
 }
 
-template <int WPB, int MINB>
-__global__ void __launch_bounds__(32 * WPB, MINB) ax8m(const __grid_constant__ hx_axlocal_args a) {
-  __shared__ ElemGeo s_g[WPB];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t e = (int64_t)blockIdx.x * WPB + w;
-  if (e >= a.n_elements) return;  // no block-wide barrier below
-  const int g = lane >> 2, q = lane & 3;
-  ElemGeo& S = s_g[w];
-
-  if (lane == 0) {
-    const int64_t ahead = e + (int64_t)148 * WPB * MINB * HX_MMA_AHEAD_WAVES4 / 4;
-    if (ahead < a.n_elements) {
-      bulk_prefetch_l2(a.x + ahead * N3, 4096u);
-      bulk_prefetch_l2(a.verts + ahead * 24, 192u);
-    }
-  }
-  const double* xe = a.x + e * N3;
-  double xa[8], xb[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(xe + k * 64 + g * 8 + 2 * q));
-    xa[k] = v.x;
-    xb[k] = v.y;
-  }
-  double Dr[2], Ds[2], Dt[2], Dy[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    Dr[s] = g_D8[g * 8 + 2 * q + s];
-    Ds[s] = g_D8[g * 8 + q + 4 * s];
-    Dt[s] = g_D8[(2 * q + s) * 8 + g];
-    Dy[s] = g_D8[(q + 4 * s) * 8 + g];
-  }
-  const double* vg = a.verts + e * 24;
-  stage_a2(lane, vg, S);
-  stage_a2(lane + 32, vg, S);
-  stage_a2(lane + 64, vg, S);
-  __syncwarp();
+// Shared by the trilinear policies: the K00 / K11 tables and the two fibres.
+template <bool DET>
+__device__ __forceinline__ void tri_prepare(ElemGeo& S, const Lane& L, TriFibre f[2]) {
+  const int g = L.g, q = L.q;
   double br[3], sr[3], U[3], V[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -396,90 +240,434 @@ __global__ void __launch_bounds__(32 * WPB, MINB) ax8m(const __grid_constant__ h
       cr[c] = fma(tk, sr[c], br[c]);
       cs[c] = fma(tk, S.ib[g][3 + c], S.ib[g][c]);
     }
-    S.t00[kk][g] = fast::dot3(cr, cr);
-    S.t11[kk][g] = fast::dot3(cs, cs);
+    S.t00[kk][g] = dot3(cr, cr);
+    S.t11[kk][g] = dot3(cs, cs);
   }
   const double aj = 8.0 * S.iw[g];
-  Fibre2 f0, f1;
-  prepare_fibre2(S, br, sr, U, V, aj, 2 * q, f0);
-  prepare_fibre2(S, br, sr, U, V, aj, 2 * q + 1, f1);
-  __syncwarp();
+  tri_fibre<DET>(S, br, sr, U, V, aj, 2 * q, f[0]);
+  tri_fibre<DET>(S, br, sr, U, V, aj, 2 * q + 1, f[1]);
+}
 
+// Trilinear recompute, Poisson or Helmholtz (axlocal.py:191-201).
+template <bool HELM>
+struct Tri {
+  static constexpr bool kTri = true, kWFold = true, kGather = !HELM;
+  TriFibre f[2];
+  const double* lam0;  // (E, n3) fields or null (scalars)
+  const double* lam1;
+  double l0v, l1v, cm[2];
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, ElemGeo& S, const Lane& L) {
+    tri_prepare<true>(S, L, f);
+    if (HELM) {
+      lam0 = a.lam0 ? a.lam0 + L.e * N3 : nullptr;
+      lam1 = a.lam1 ? a.lam1 + L.e * N3 : nullptr;
+      l0v = a.lam0_value;
+      l1v = a.lam1_value;
+      // mass = lam1 lam_geo det^2 / 64 = w_k lam1 det' (0.125 w_j w_i)^2 / 64
+      const double wj = fast::wr(L.g);
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double wji8 = 0.125 * (wj * fast::wr(2 * L.q + b));
+        cm[b] = 0.015625 * (wji8 * wji8);
+      }
+    }
+  }
+  template <int K>
+  __device__ __forceinline__ void slice(const ElemGeo& S, const Lane& L, const double x0[2], const double x1[2],
+                                        const double x2[2], const double xk[2], double rr[2], double ss[2],
+                                        double tt[2], double ms[2]) const {
+    const double a00 = S.t00[K][L.g];
+    const double2 a11 = *reinterpret_cast<const double2*>(&S.t11[K][2 * L.q]);
+    double2 l0 = make_double2(l0v, l0v), l1 = make_double2(l1v, l1v);
+    const int n = K * 64 + L.g * 8 + 2 * L.q;
+    if (HELM && lam0) l0 = ld2(lam0 + n);
+    if (HELM && lam1) l1 = ld2(lam1 + n);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      double g[6], dt;
+      tri_adj<K>(f[b], a00, b ? a11.y : a11.x, g);
+      double sc = tri_rdet<K>(f[b], dt);
+      if (HELM) {
+        ms[b] = ((b ? l1.y : l1.x) * (dt * cm[b])) * xk[b];
+        sc = (b ? l0.y : l0.x) * sc;
+      }
+      symv(g[0], g[1], g[2], g[3], g[4], g[5], sc, x0[b], x1[b], x2[b], rr[b], ss[b], tt[b]);
+    }
+  }
+};
+
+// Trilinear with a stored per-node scale: partial (Poisson, lam_geo) or
+// merged (Helmholtz, lam2 / lam3) -- the stored scales carry w_k (no folding).
+template <bool MERGED>
+struct TriStoredScale {
+  static constexpr bool kTri = true, kWFold = false, kGather = !MERGED;
+  TriFibre f[2];
+  const double* sa;  // lam_geo or lam2
+  const double* sb;  // lam3
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, ElemGeo& S, const Lane& L) {
+    tri_prepare<false>(S, L, f);
+    sa = (MERGED ? a.lam2 : a.lam_geo) + L.e * N3;
+    sb = MERGED ? a.lam3 + L.e * N3 : nullptr;
+  }
+  template <int K>
+  __device__ __forceinline__ void slice(const ElemGeo& S, const Lane& L, const double x0[2], const double x1[2],
+                                        const double x2[2], const double xk[2], double rr[2], double ss[2],
+                                        double tt[2], double ms[2]) const {
+    const double a00 = S.t00[K][L.g];
+    const double2 a11 = *reinterpret_cast<const double2*>(&S.t11[K][2 * L.q]);
+    const int n = K * 64 + L.g * 8 + 2 * L.q;
+    const double2 s2 = ld2(sa + n);
+    double2 m2 = make_double2(0.0, 0.0);
+    if (MERGED) m2 = ld2(sb + n);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      double g[6];
+      tri_adj<K>(f[b], a00, b ? a11.y : a11.x, g);
+      symv(g[0], g[1], g[2], g[3], g[4], g[5], b ? s2.y : s2.x, x0[b], x1[b], x2[b], rr[b], ss[b], tt[b]);
+      if (MERGED) ms[b] = (b ? m2.y : m2.x) * xk[b];
+    }
+  }
+};
+
+// Parallelepiped: g = w (x) h (geometry.py:389-398), w_j w_i per fibre, w_k folded.
+template <bool HELM>
+struct Ppd {
+  static constexpr bool kTri = false, kWFold = true, kGather = false;
+  double h[7], wji[2];
+  const double* lam0;
+  const double* lam1;
+  double l0v, l1v;
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, ElemGeo&, const Lane& L) {
+#pragma unroll
+    for (int c = 0; c < 7; ++c) h[c] = __ldg(a.h + L.e * 7 + c);
+    const double wj = fast::wr(L.g);
+    wji[0] = wj * fast::wr(2 * L.q);
+    wji[1] = wj * fast::wr(2 * L.q + 1);
+    if (HELM) {
+      lam0 = a.lam0 ? a.lam0 + L.e * N3 : nullptr;
+      lam1 = a.lam1 ? a.lam1 + L.e * N3 : nullptr;
+      l0v = a.lam0_value;
+      l1v = a.lam1_value;
+    }
+  }
+  template <int K>
+  __device__ __forceinline__ void slice(const ElemGeo&, const Lane& L, const double x0[2], const double x1[2],
+                                        const double x2[2], const double xk[2], double rr[2], double ss[2],
+                                        double tt[2], double ms[2]) const {
+    double2 l0 = make_double2(l0v, l0v), l1 = make_double2(l1v, l1v);
+    const int n = K * 64 + L.g * 8 + 2 * L.q;
+    if (HELM && lam0) l0 = ld2(lam0 + n);
+    if (HELM && lam1) l1 = ld2(lam1 + n);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      symv(h[0], h[1], h[2], h[3], h[4], h[5], wji[b], x0[b], x1[b], x2[b], rr[b], ss[b], tt[b]);
+      if (HELM) {
+        const double l = b ? l0.y : l0.x;
+        rr[b] *= l;
+        ss[b] *= l;
+        tt[b] *= l;
+        ms[b] = ((b ? l1.y : l1.x) * (wji[b] * h[6])) * xk[b];
+      }
+    }
+  }
+};
+
+// Stored (Nek-style) factors: 6 (+gwj) SoA loads per node (axlocal.py:181-185).
+template <bool HELM>
+struct Stored {
+  static constexpr bool kTri = false, kWFold = false, kGather = false;
+  const double* gp;
+  const double* gwj;
+  const double* lam0;
+  const double* lam1;
+  double l0v, l1v;
+  __device__ __forceinline__ void prepare(const hx_axlocal_args& a, ElemGeo&, const Lane& L) {
+    gp = a.g + L.e * 6 * N3;
+    if (HELM) {
+      gwj = a.gwj + L.e * N3;
+      lam0 = a.lam0 ? a.lam0 + L.e * N3 : nullptr;
+      lam1 = a.lam1 ? a.lam1 + L.e * N3 : nullptr;
+      l0v = a.lam0_value;
+      l1v = a.lam1_value;
+    }
+  }
+  template <int K>
+  __device__ __forceinline__ void slice(const ElemGeo&, const Lane& L, const double x0[2], const double x1[2],
+                                        const double x2[2], const double xk[2], double rr[2], double ss[2],
+                                        double tt[2], double ms[2]) const {
+    const int n = K * 64 + L.g * 8 + 2 * L.q;
+    double2 gg[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) gg[c] = ld2(gp + c * N3 + n);
+    double2 l0 = make_double2(l0v, l0v), l1 = make_double2(l1v, l1v), gw = make_double2(0.0, 0.0);
+    if (HELM) {
+      if (lam0) l0 = ld2(lam0 + n);
+      if (lam1) l1 = ld2(lam1 + n);
+      gw = ld2(gwj + n);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double g0 = b ? gg[0].y : gg[0].x, g1 = b ? gg[1].y : gg[1].x, g2 = b ? gg[2].y : gg[2].x;
+      const double g3 = b ? gg[3].y : gg[3].x, g4 = b ? gg[4].y : gg[4].x, g5 = b ? gg[5].y : gg[5].x;
+      rr[b] = fma(g0, x0[b], fma(g1, x1[b], g2 * x2[b]));
+      ss[b] = fma(g1, x0[b], fma(g3, x1[b], g4 * x2[b]));
+      tt[b] = fma(g2, x0[b], fma(g4, x1[b], g5 * x2[b]));
+      if (HELM) {
+        const double l = b ? l0.y : l0.x;
+        rr[b] *= l;
+        ss[b] *= l;
+        tt[b] *= l;
+        ms[b] = ((b ? l1.y : l1.x) * (b ? gw.y : gw.x)) * xk[b];
+      }
+    }
+  }
+};
+
+#ifndef HX_MMA_AHEAD_WAVES4
+#define HX_MMA_AHEAD_WAVES4 5  // L2 prefetch distance in quarter waves of resident warps
+#endif
+
+// Where a column's x comes from: element-local (E, n1^3, NCOL), or (GATHER)
+// the slab lattice of the fused BP5 gather -- node (i,j,k) of element (cx,cy,cz)
+// is lattice point (7 cx + i, 7 cy + j, 7 cz + k), the index computed, not
+// loaded -- optionally (CGP) with the CG direction update p = r + beta p_old
+// applied on the fly (the rounding of cg_p_kernel, solver.py:170) and the
+// thread's own nodes of p written to cg_p_out.
+template <int NCOL, bool GATHER, bool CGP>
+struct XSrc {
+  const double* x;
+  const double* r;
+  double* pout;
+  int64_t sk, sj;  // strides of k and j (i stride: NCOL, or 1 on the lattice)
+  double beta;
+  __device__ __forceinline__ XSrc(const hx_axlocal_args& a, const Lane& L, int col) {
+    if (GATHER) {
+      const hx_box& bx = a.gather_box;
+      const int64_t nx = (int64_t)bx.ex * 7 + 1, ny = (int64_t)bx.ey * 7 + 1;
+      const unsigned e32 = (unsigned)L.e, exu = (unsigned)bx.ex, exy = exu * (unsigned)bx.ey;
+      const unsigned cz = e32 / exy, rem = e32 - cz * exy, cy = rem / exu, cx = rem - cy * exu;
+      const int64_t base = ((int64_t)(cz * 7) * ny + cy * 7) * nx + cx * 7;
+      x = a.x + base;
+      sk = nx * ny;
+      sj = nx;
+      if (CGP) {
+        r = a.cg_r + base;
+        pout = a.cg_p_out + base;
+        beta = a.cg_scal[2] / a.cg_scal[0];
+      }
+    } else {
+      x = a.x + L.e * N3 * NCOL + col;
+      sk = 64 * NCOL;
+      sj = 8 * NCOL;
+    }
+  }
+  __device__ __forceinline__ int64_t off(int k, int j, int i) const {
+    return k * sk + j * sj + (GATHER ? i : i * NCOL);
+  }
+  __device__ __forceinline__ double at(int k, int j, int i) const {
+    const int64_t o = off(k, j, i);
+    if (CGP) return __dadd_rn(__ldg(r + o), __dmul_rn(beta, __ldg(x + o)));
+    return __ldg(x + o);
+  }
+  // the thread's pair of nodes (k, j, i), (k, j, i + 1)
+  __device__ __forceinline__ void pair(int k, int j, int i, double& v0, double& v1) const {
+    if (NCOL == 1 && !GATHER) {
+      const double2 v = ld2(x + off(k, j, i));
+      v0 = v.x;
+      v1 = v.y;
+    } else {
+      v0 = at(k, j, i);
+      v1 = at(k, j, i + 1);
+      if (CGP) {
+        const int64_t o = off(k, j, i);
+        pout[o] = v0;
+        pout[o + 1] = v1;
+      }
+    }
+  }
+};
+
+// One column of one element: x -> y, with the geometry prepared.
+template <typename F, int NCOL, bool GATHER = false, bool CGP = false>
+__device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, const F& fac, const Lane& L,
+                                       const double Dr[2], const double Ds[2], const double Dt[2],
+                                       const double Dy[2], int col) {
+  const int g = L.g, q = L.q;
+  const XSrc<NCOL, GATHER, CGP> X(a, L, col);
+  double xa[8], xb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) X.pair(k, g, 2 * q, xa[k], xb[k]);
   double ta[8], tb[8];
   fast::eo8<0>(xa, ta);
   fast::eo8<0>(xb, tb);
 
-#define HX_SLICE(K)                                                                                \
-  {                                                                                                \
-    double r0, r1, s0, s1;                                                                         \
-    dmma(r0, r1, xa[K], Dr[0], 0.0, 0.0);                                                          \
-    dmma(r0, r1, xb[K], Dr[1], r0, r1);                                                            \
-    const double bx0 = __ldg(xe + K * 64 + q * 8 + g), bx1 = __ldg(xe + K * 64 + (q + 4) * 8 + g); \
-    dmma(s0, s1, Ds[0], bx0, 0.0, 0.0);                                                            \
-    dmma(s0, s1, Ds[1], bx1, s0, s1);                                                              \
-    const double a00 = S.t00[K][g];                                                                \
-    const double2 a11 = *reinterpret_cast<const double2*>(&S.t11[K][2 * q]);                       \
-    double rr0, ss0, rr1, ss1;                                                                     \
-    tri_node2<K>(f0, a00, a11.x, r0, s0, ta[K], rr0, ss0, ta[K]);                                  \
-    tri_node2<K>(f1, a00, a11.y, r1, s1, tb[K], rr1, ss1, tb[K]);                                  \
-    double* tl = S.tile[K & 1];                                                                    \
-    *reinterpret_cast<double2*>(tl + g * 8 + 2 * q) = make_double2(ss0, ss1);                      \
-    __syncwarp();                                                                                  \
-    double y0, y1;                                                                                 \
-    dmma(y0, y1, rr0, Dt[0], 0.0, 0.0);                                                            \
-    dmma(y0, y1, rr1, Dt[1], y0, y1);                                                              \
-    dmma(y0, y1, Dy[0], tl[q * 8 + g], y0, y1);                                                    \
-    dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);                                              \
-    xa[K] = y0;                                                                                    \
-    xb[K] = y1;                                                                                    \
+#define HX_SLICE(K)                                                                                    \
+  {                                                                                                    \
+    double x0[2], x1[2], x2[2] = {ta[K], tb[K]}, xk[2] = {xa[K], xb[K]};                               \
+    dmma(x0[0], x0[1], xa[K], Dr[0], 0.0, 0.0);                                                        \
+    dmma(x0[0], x0[1], xb[K], Dr[1], x0[0], x0[1]);                                                    \
+    const double bx0 = X.at(K, q, g), bx1 = X.at(K, q + 4, g);                                          \
+    dmma(x1[0], x1[1], Ds[0], bx0, 0.0, 0.0);                                                          \
+    dmma(x1[0], x1[1], Ds[1], bx1, x1[0], x1[1]);                                                      \
+    double rr[2], ss[2], tt[2], ms[2] = {0.0, 0.0};                                                    \
+    fac.template slice<K>(S, L, x0, x1, x2, xk, rr, ss, tt, ms);                                       \
+    ta[K] = tt[0];                                                                                     \
+    tb[K] = tt[1];                                                                                     \
+    double* tl = S.tile[K & 1];                                                                        \
+    *reinterpret_cast<double2*>(tl + g * 8 + 2 * q) = make_double2(ss[0], ss[1]);                      \
+    __syncwarp();                                                                                      \
+    double y0, y1;                                                                                     \
+    dmma(y0, y1, rr[0], Dt[0], ms[0], ms[1]);                                                          \
+    dmma(y0, y1, rr[1], Dt[1], y0, y1);                                                                \
+    dmma(y0, y1, Dy[0], tl[q * 8 + g], y0, y1);                                                        \
+    dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);                                                  \
+    xa[K] = y0;                                                                                        \
+    xb[K] = y1;                                                                                        \
   }
   HX_SLICE(0) HX_SLICE(1) HX_SLICE(2) HX_SLICE(3) HX_SLICE(4) HX_SLICE(5) HX_SLICE(6) HX_SLICE(7)
 #undef HX_SLICE
 
   double ya[8], yb[8];
-  eo8w(ta, ya);
-  eo8w(tb, yb);
-  double* ye = a.y + e * N3;
+  if (F::kWFold) {
+    eo8w(ta, ya);
+    eo8w(tb, yb);
+  } else {
+    fast::eo8<1>(ta, ya);
+    fast::eo8<1>(tb, yb);
+  }
+  double* ye = a.y + L.e * N3 * NCOL + col;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const double wk = cW<N1>(k);
-    *reinterpret_cast<double2*>(ye + k * 64 + g * 8 + 2 * q) =
-        make_double2(fma(wk, xa[k], ya[k]), fma(wk, xb[k], yb[k]));
+    double y0, y1;
+    if (F::kWFold) {
+      const double wk = cW<N1>(k);
+      y0 = fma(wk, xa[k], ya[k]);
+      y1 = fma(wk, xb[k], yb[k]);
+    } else {
+      y0 = xa[k] + ya[k];
+      y1 = xb[k] + yb[k];
+    }
+    const int n = k * 64 + g * 8 + 2 * q;
+    if (NCOL == 1) {
+      *reinterpret_cast<double2*>(ye + n) = make_double2(y0, y1);
+    } else {
+      ye[n * NCOL] = y0;
+      ye[(n + 1) * NCOL] = y1;
+    }
   }
 }
 
-template <int WPB, int MINB, int V = 2>
+template <typename F, int NCOL, int MINB, bool GATHER = false, bool CGP = false>
+__global__ void __launch_bounds__(32, MINB) ax8m(const __grid_constant__ hx_axlocal_args a) {
+  __shared__ ElemGeo S;
+  const int lane = threadIdx.x;
+  // n_col = 3: one warp per (element, column), each the n_col = 1 arithmetic
+  const int col = NCOL == 1 ? 0 : (int)(blockIdx.x % NCOL);
+  Lane L;
+  L.e = NCOL == 1 ? (int64_t)blockIdx.x : (int64_t)(blockIdx.x / NCOL);
+  L.g = lane >> 2;
+  L.q = lane & 3;
+
+  // warm L2 with the element ~1.25 waves of resident warps ahead: x, vertices,
+  // and the per-node fields of the variants that stream them
+  if (lane < 2 && col == 0) {
+    const int64_t ahead = L.e + (int64_t)148 * MINB * HX_MMA_AHEAD_WAVES4 / 4 / NCOL;
+    if (ahead < a.n_elements) {
+      if (lane == 0) {
+        if (!GATHER) bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
+        if (F::kTri) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
+      } else {
+        if (a.lam_geo) bulk_prefetch_l2(a.lam_geo + ahead * N3, 4096u);
+        if (a.lam2) bulk_prefetch_l2(a.lam2 + ahead * N3, 4096u);
+        if (a.lam3) bulk_prefetch_l2(a.lam3 + ahead * N3, 4096u);
+        if (a.lam0) bulk_prefetch_l2(a.lam0 + ahead * N3, 4096u);
+        if (a.lam1) bulk_prefetch_l2(a.lam1 + ahead * N3, 4096u);
+      }
+    }
+  }
+  if (GATHER) {
+    // fused gather: warm the 64 lattice rows (64 B each) of the element ahead, two per lane
+    const int64_t ahead = L.e + (int64_t)148 * MINB * HX_MMA_AHEAD_WAVES4 / 4;
+    if (ahead < a.n_elements) {
+      Lane La = L;
+      La.e = ahead;
+      const XSrc<1, true, false> Xa(a, La, 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = 2 * lane + h;
+        prefetch_l2(Xa.x + Xa.off(row >> 3, row & 7, 0));
+        if (CGP) prefetch_l2(a.cg_r + (Xa.x - a.x) + Xa.off(row >> 3, row & 7, 0));
+      }
+    }
+  }
+  double Dr[2], Ds[2], Dt[2], Dy[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    Dr[s] = g_D8[L.g * 8 + 2 * L.q + s];
+    Ds[s] = g_D8[L.g * 8 + L.q + 4 * s];
+    Dt[s] = g_D8[(2 * L.q + s) * 8 + L.g];
+    Dy[s] = g_D8[(L.q + 4 * s) * 8 + L.g];
+  }
+  if (F::kTri) {
+    const double* vg = a.verts + L.e * 24;
+    stage_a(lane, vg, S);
+    stage_a(lane + 32, vg, S);
+    stage_a(lane + 64, vg, S);
+    __syncwarp();
+  }
+  F fac;
+  fac.prepare(a, S, L);
+  if (F::kTri) __syncwarp();
+  column<F, NCOL, GATHER, CGP>(a, S, fac, L, Dr, Ds, Dt, Dy, col);
+}
+
+template <typename F, int MINB = 12>
 cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
-  const int64_t blocks = (a.n_elements + WPB - 1) / WPB;
-  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  if (V == 1)
-    ax8m_v1<WPB, MINB><<<(unsigned)blocks, 32 * WPB, 0, s>>>(a);
+  if (a.n_elements * a.n_col > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)(a.n_elements * a.n_col);
+  if (a.gather) {  // n_col = 1 (checked by hx_axlocal)
+    if constexpr (F::kGather) {
+      if (a.cg_r)
+        ax8m<F, 1, MINB, true, true><<<grid, 32, 0, s>>>(a);
+      else
+        ax8m<F, 1, MINB, true><<<grid, 32, 0, s>>>(a);
+    } else {
+      return cudaErrorNotSupported;
+    }
+  } else if (a.n_col == 3)
+    ax8m<F, 3, MINB><<<grid, 32, 0, s>>>(a);
   else
-    ax8m<WPB, MINB><<<(unsigned)blocks, 32 * WPB, 0, s>>>(a);
+    ax8m<F, 1, MINB><<<grid, 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 }  // namespace mma
 }  // namespace hx
 
-// Trilinear Poisson, n_col = 1, element-local x (no fused gather); 16-byte
-// aligned x / y.  Returns cudaErrorNotSupported for anything else.
+// Every (equation, factor source, n_col) at order 7 with element-local x and
+// 16-byte aligned x / y, and the fused lattice gather (+ CG update) for the
+// Poisson trilinear / trilinear-partial sources; cudaErrorNotSupported otherwise.
 extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
   using namespace hx::mma;
-  if (a->order != 7 || a->n_col != 1 || a->gather || a->equation != HX_POISSON ||
-      a->factor_source != HX_TRILINEAR)
+  if (a->order != 7) return cudaErrorNotSupported;
+  if (((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->y)) & (a->gather ? 7u : 15u)) != 0)
     return cudaErrorNotSupported;
-  if (((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->y)) & 15u) != 0)
-    return cudaErrorNotSupported;
-  switch (a->reserved) {
-    case 41: return launch<1, 12>(*a, s);
-    case 42: return launch<2, 8>(*a, s);
-    case 43: return launch<4, 3>(*a, s);
-    case 44: return launch<4, 4>(*a, s);
-    case 45: return launch<1, 12, 1>(*a, s);
-    case 46: return launch<2, 6>(*a, s);
-    default: return launch<1, 12>(*a, s);
+  const bool helm = a->equation == HX_HELMHOLTZ;
+  if (a->gather && (helm || (a->factor_source != HX_TRILINEAR && a->factor_source != HX_TRILINEAR_PARTIAL)))
+    return cudaErrorNotSupported;  // the lattice gather is built for the trilinear Poisson sources
+  switch (a->factor_source) {
+    case HX_TRILINEAR:
+      return helm ? launch<Tri<true>>(*a, s) : launch<Tri<false>>(*a, s);
+    case HX_TRILINEAR_PARTIAL:
+      return launch<TriStoredScale<false>>(*a, s);
+    case HX_TRILINEAR_MERGED:
+      return launch<TriStoredScale<true>>(*a, s);
+    case HX_PARALLELEPIPED:
+      return helm ? launch<Ppd<true>>(*a, s) : launch<Ppd<false>>(*a, s);
+    case HX_STORED:
+      return helm ? launch<Stored<true>>(*a, s) : launch<Stored<false>>(*a, s);
   }
+  return cudaErrorNotSupported;
 }
 
 extern "C" cudaError_t hx_upload_basis_mma(int n1, const double* pts, const double* w, const double* d) {

@@ -20,10 +20,18 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("no CUDA device", allow_module_level=True)
 
 DEV = torch.device("cuda", 0)
-KERNELS = (0, 1, 2)  # 0 = best measured, 1 = slice kernel (Algorithm 4), 2 = fast kernel (specialised / order-generic)
+# 0 = best measured, 1 = slice kernel (Algorithm 4), 2 = fast kernel (specialised / order-generic),
+# 4 = DMMA kernel (order 7 only, ax_mma.cu)
+KERNELS = (0, 1, 2, 4)
+
+
+def _need(kernel, order):
+    if kernel == 4 and order != 7:
+        pytest.skip("kernel 4 (DMMA) covers order 7")
 
 
 def _op(c, elements, kernel):
+    _need(kernel, c["order"])
     spec = hx.KernelSpec(c["equation"], c["n_col"], c["source"], c["order"])
     op = hx.LocalOperator(spec, elements, hx.SpectralBasis.build(c["order"]), lam0=c["lam0"], lam1=c["lam1"])
     op.kernel = kernel
@@ -61,6 +69,7 @@ def _random_box(order, ex, ey, ez, pert=0.1, seed=0):
 @pytest.mark.parametrize("order", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15])
 def test_every_order_trilinear_and_stored(order, kernel):
     """All orders N=1..15 (config C3's sweep) on a perturbed box, vs the oracle."""
+    _need(kernel, order)
     mesh = _random_box(order, 3, 2, 2, pert=0.15, seed=order)
     rng = np.random.default_rng(order)
     x = rng.standard_normal((mesh.n_elements, (order + 1) ** 3, 1))
@@ -75,6 +84,7 @@ def test_every_order_trilinear_and_stored(order, kernel):
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("order", [3, 7, 11])
 def test_every_variant_helmholtz_ncol3(order, kernel):
+    _need(kernel, order)
     mesh = _random_box(order, 2, 2, 2, pert=0.2, seed=3)
     E, n3 = mesh.n_elements, (order + 1) ** 3
     rng = np.random.default_rng(5)
@@ -94,6 +104,7 @@ def test_every_variant_helmholtz_ncol3(order, kernel):
 @pytest.mark.parametrize("order", [2, 7])
 def test_parallelepiped_sheared_box(order, kernel):
     """Axis-aligned boxes would hide off-diagonal factor bugs: shear the box."""
+    _need(kernel, order)
     mesh = hx.box_mesh(3, 2, 2, order)
     shear = np.array([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]])
     verts = mesh.vertices @ shear.T
@@ -178,10 +189,17 @@ def test_ncol3_bitwise_equals_three_ncol1(kernel):
     mesh = _random_box(order, 4, 3, 2, seed=9)
     rng = np.random.default_rng(1)
     x = torch.as_tensor(rng.standard_normal((mesh.n_elements, 512, 3)), device=DEV)
+    shear = np.array([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]])
+    ppd = torch.as_tensor(hx.box_mesh(4, 3, 2, order).vertices @ shear.T, device=DEV)
+    E = mesh.n_elements
+    kw = {"lam0": rng.uniform(0.5, 2.0, (E, 512)), "lam1": rng.uniform(0.5, 2.0, (E, 512))}
     for eq, src in (("poisson", "trilinear"), ("poisson", "stored"), ("helmholtz", "trilinear-merged"),
-                    ("poisson", "trilinear-partial")):
-        op3 = hx.LocalOperator(hx.KernelSpec(eq, 3, src, order), mesh, hx.SpectralBasis.build(order))
-        op1 = hx.LocalOperator(hx.KernelSpec(eq, 1, src, order), mesh, hx.SpectralBasis.build(order))
+                    ("poisson", "trilinear-partial"), ("helmholtz", "trilinear"), ("helmholtz", "stored"),
+                    ("poisson", "parallelepiped"), ("helmholtz", "parallelepiped")):
+        els = ppd if src == "parallelepiped" else mesh
+        k = kw if eq == "helmholtz" else {}
+        op3 = hx.LocalOperator(hx.KernelSpec(eq, 3, src, order), els, hx.SpectralBasis.build(order), **k)
+        op1 = hx.LocalOperator(hx.KernelSpec(eq, 1, src, order), els, hx.SpectralBasis.build(order), **k)
         op3.kernel = op1.kernel = kernel
         y3 = op3.apply(x)
         for c in range(3):
@@ -365,13 +383,13 @@ def test_apply_inplace_validates_buffers():
             op.apply_(x, bad)
 
 
-@pytest.mark.parametrize("order", [1, 2, 3, 5, 6, 8, 9, 12, 15])
+@pytest.mark.parametrize("order", [1, 2, 3, 5, 6, 7, 8, 9, 12, 15])
 def test_every_family_is_deterministic(order):
     """Shared-memory races show up as run-to-run differences: every kernel family,
     n_col 1 and 3, three applies each, bitwise equal (and all families agree to 1e-12)."""
     mesh = _random_box(order, 5, 3, 2, pert=0.15, seed=order)
     n3 = (order + 1) ** 3
-    kernels = (0, 1, 2, 3) if order <= 2 else (0, 1, 2)
+    kernels = (0, 1, 2, 3) if order <= 2 else (0, 1, 2, 4) if order == 7 else (0, 1, 2)
     for eq, src, ncol in (("poisson", "trilinear", 1), ("helmholtz", "stored", 3), ("poisson", "trilinear-partial", 3)):
         kw = {"lam0": 1.1, "lam1": 0.7} if eq == "helmholtz" else {}
         x = torch.randn((mesh.n_elements, n3, ncol), dtype=torch.float64, device=DEV)
