@@ -45,6 +45,11 @@
 // D (row-major [i][m]) for the per-lane fragments (lane-dependent indices: a
 // global array read once per warp through L1, not a divergent constant load).
 static __device__ double g_D8[64];
+// GLL points and inverse weights for lane-dependent indices (one L1 load each,
+// instead of the select chains of fast::pick8)
+static __device__ double g_X8[8];
+static __device__ double g_W8[8];
+static __device__ double g_IW8[8];
 
 namespace hx {
 namespace mma {
@@ -53,7 +58,6 @@ using fast::N1;
 using fast::N3;
 
 static __constant__ double c_EOW[2][4][4];  // D^T even-odd blocks, column m scaled by w_m
-static __constant__ double c_IW[8];         // 1 / w_m
 
 // D = A B + C, m8n8k4 f64: A [g][q], B [q][g], C/D [g][2q], [g][2q+1].
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b, double c0, double c1) {
@@ -79,7 +83,7 @@ struct ElemGeo {
 __device__ __forceinline__ void stage_a(int t, const double* __restrict__ v, ElemGeo& s) {
   if (t < 72) {
     const int side = t / 24, task = t - 24 * side, idx = task / 3, c = task % 3;
-    const double xi = fast::xr(idx);
+    const double xi = g_X8[idx];
     const double a0 = 1.0 - xi, a1 = 1.0 + xi;
     // j side: a0 (v1-v0) + a1 (v3-v2) | a0 (v5-v4) + a1 (v7-v6)   (geometry.py:152-167)
     // i side: a0 (v2-v0) + a1 (v3-v1) | a0 (v6-v4) + a1 (v7-v5)
@@ -94,8 +98,8 @@ __device__ __forceinline__ void stage_a(int t, const double* __restrict__ v, Ele
     out[c] = lo + hi;
     out[3 + c] = hi - lo;
   } else if (t < 80) {
-    s.xs[t - 72] = fast::xr(t - 72);
-    s.iw[t - 72] = fast::pick8(c_IW, t - 72);
+    s.xs[t - 72] = g_X8[t - 72];
+    s.iw[t - 72] = g_IW8[t - 72];
   }
 }
 
@@ -218,40 +222,46 @@ __device__ __forceinline__ double tri_rdet(const TriFibre& f, double& dt) {
   return fma(fma(e, e, e), r, r);
 }
 
-// Shared by the trilinear policies: the K00 / K11 tables and the two fibres.
+// K00(j = jj, k = kk) and K11(i = jj, k = kk) table entries.
+__device__ __forceinline__ void tri_tables(ElemGeo& S, int jj, int kk) {
+  const double tk = S.xs[kk];
+  double cr[3], cs[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    cr[c] = fma(tk, S.jb[jj][3 + c], S.jb[jj][c]);
+    cs[c] = fma(tk, S.ib[jj][3 + c], S.ib[jj][c]);
+  }
+  S.t00[kk][jj] = dot3(cr, cr);
+  S.t11[kk][jj] = dot3(cs, cs);
+}
+
+// Fibre (j = g, i = 2q + b).
 template <bool DET>
-__device__ __forceinline__ void tri_prepare(ElemGeo& S, const Lane& L, TriFibre f[2]) {
-  const int g = L.g, q = L.q;
+__device__ __forceinline__ void tri_fibre_of(const ElemGeo& S, const Lane& L, int b, TriFibre& f) {
   double br[3], sr[3], U[3], V[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    br[c] = S.jb[g][c];
-    sr[c] = S.jb[g][3 + c];
-    U[c] = S.uv[g][c];
-    V[c] = S.uv[g][3 + c];
+    br[c] = S.jb[L.g][c];
+    sr[c] = S.jb[L.g][3 + c];
+    U[c] = S.uv[L.g][c];
+    V[c] = S.uv[L.g][3 + c];
   }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int kk = 2 * q + h;
-    const double tk = S.xs[kk];
-    double cr[3], cs[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      cr[c] = fma(tk, sr[c], br[c]);
-      cs[c] = fma(tk, S.ib[g][3 + c], S.ib[g][c]);
-    }
-    S.t00[kk][g] = dot3(cr, cr);
-    S.t11[kk][g] = dot3(cs, cs);
-  }
-  const double aj = 8.0 * S.iw[g];
-  tri_fibre<DET>(S, br, sr, U, V, aj, 2 * q, f[0]);
-  tri_fibre<DET>(S, br, sr, U, V, aj, 2 * q + 1, f[1]);
+  tri_fibre<DET>(S, br, sr, U, V, 8.0 * S.iw[L.g], 2 * L.q + b, f);
+}
+
+// Shared by the trilinear policies: the K00 / K11 tables and the two fibres.
+template <bool DET>
+__device__ __forceinline__ void tri_prepare(ElemGeo& S, const Lane& L, TriFibre f[2]) {
+  tri_tables(S, L.g, 2 * L.q);
+  tri_tables(S, L.g, 2 * L.q + 1);
+  tri_fibre_of<DET>(S, L, 0, f[0]);
+  tri_fibre_of<DET>(S, L, 1, f[1]);
 }
 
 // Trilinear recompute, Poisson or Helmholtz (axlocal.py:191-201).
 template <bool HELM>
 struct Tri {
-  static constexpr bool kTri = true, kWFold = true, kGather = !HELM;
+  static constexpr bool kTri = true, kWFold = true, kGather = !HELM, kFields = HELM;
   TriFibre f[2];
   const double* lam0;  // (E, n3) fields or null (scalars)
   const double* lam1;
@@ -264,10 +274,9 @@ struct Tri {
       l0v = a.lam0_value;
       l1v = a.lam1_value;
       // mass = lam1 lam_geo det^2 / 64 = w_k lam1 det' (0.125 w_j w_i)^2 / 64
-      const double wj = fast::wr(L.g);
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
-        const double wji8 = 0.125 * (wj * fast::wr(2 * L.q + b));
+        const double wji8 = 0.125 * (g_W8[L.g] * g_W8[2 * L.q + b]);
         cm[b] = 0.015625 * (wji8 * wji8);
       }
     }
@@ -294,13 +303,46 @@ struct Tri {
       symv(g[0], g[1], g[2], g[3], g[4], g[5], sc, x0[b], x1[b], x2[b], rr[b], ss[b], tt[b]);
     }
   }
+
+  // n_col = 3 factor reuse (ax8m3): the same arithmetic split into the per-node
+  // factors (g, scale[, mass coefficient]) and their application to one column.
+  static constexpr int kNF = HELM ? 8 : 7;
+  __device__ __forceinline__ void prepare_one(const hx_axlocal_args& a, const ElemGeo& S, const Lane& L, int b) {
+    tri_fibre_of<true>(S, L, b, f[b]);
+    if (HELM) {
+      lam0 = a.lam0 ? a.lam0 + L.e * N3 : nullptr;
+      lam1 = a.lam1 ? a.lam1 + L.e * N3 : nullptr;
+      l0v = a.lam0_value;
+      l1v = a.lam1_value;
+      const double wji8 = 0.125 * (g_W8[L.g] * g_W8[2 * L.q + b]);
+      cm[b] = 0.015625 * (wji8 * wji8);
+    }
+  }
+  template <int K>
+  __device__ __forceinline__ void node_factors(const ElemGeo& S, const Lane& L, int b, double v[kNF]) const {
+    double dt;
+    tri_adj<K>(f[b], S.t00[K][L.g], S.t11[K][2 * L.q + b], v);
+    double sc = tri_rdet<K>(f[b], dt);
+    if (HELM) {
+      const int n = K * 64 + L.g * 8 + 2 * L.q + b;
+      const double l0 = lam0 ? __ldg(lam0 + n) : l0v, l1 = lam1 ? __ldg(lam1 + n) : l1v;
+      v[7] = l1 * (dt * cm[b]);
+      sc = l0 * sc;
+    }
+    v[6] = sc;
+  }
+  __device__ __forceinline__ static void apply(const double v[kNF], double x0, double x1, double x2, double xk,
+                                               double& rr, double& ss, double& tt, double& ms) {
+    if (HELM) ms = v[7] * xk;
+    symv(v[0], v[1], v[2], v[3], v[4], v[5], v[6], x0, x1, x2, rr, ss, tt);
+  }
 };
 
 // Trilinear with a stored per-node scale: partial (Poisson, lam_geo) or
 // merged (Helmholtz, lam2 / lam3) -- the stored scales carry w_k (no folding).
 template <bool MERGED>
 struct TriStoredScale {
-  static constexpr bool kTri = true, kWFold = false, kGather = !MERGED;
+  static constexpr bool kTri = true, kWFold = false, kGather = !MERGED, kFields = true;
   TriFibre f[2];
   const double* sa;  // lam_geo or lam2
   const double* sb;  // lam3
@@ -327,12 +369,54 @@ struct TriStoredScale {
       if (MERGED) ms[b] = (b ? m2.y : m2.x) * xk[b];
     }
   }
+
+  static constexpr int kNF = MERGED ? 8 : 7;
+  __device__ __forceinline__ void prepare_one(const hx_axlocal_args& a, const ElemGeo& S, const Lane& L, int b) {
+    tri_fibre_of<false>(S, L, b, f[b]);
+    sa = (MERGED ? a.lam2 : a.lam_geo) + L.e * N3;
+    sb = MERGED ? a.lam3 + L.e * N3 : nullptr;
+  }
+  template <int K>
+  __device__ __forceinline__ void node_factors(const ElemGeo& S, const Lane& L, int b, double v[kNF]) const {
+    tri_adj<K>(f[b], S.t00[K][L.g], S.t11[K][2 * L.q + b], v);
+    const int n = K * 64 + L.g * 8 + 2 * L.q + b;
+    v[6] = __ldg(sa + n);
+    if (MERGED) v[7] = __ldg(sb + n);
+  }
+  __device__ __forceinline__ static void apply(const double v[kNF], double x0, double x1, double x2, double xk,
+                                               double& rr, double& ss, double& tt, double& ms) {
+    symv(v[0], v[1], v[2], v[3], v[4], v[5], v[6], x0, x1, x2, rr, ss, tt);
+    if (MERGED) ms = v[7] * xk;
+  }
+};
+
+// The per-node factors of a trilinear policy read back from shared memory
+// (ax8m3's column pass): [slice][factor][lane] pairs for the lane's two fibres.
+template <typename F>
+struct FacLoaded {
+  static constexpr bool kTri = true, kWFold = F::kWFold;
+  const double2 (*fac)[F::kNF][32];
+  template <int K>
+  __device__ __forceinline__ void slice(const ElemGeo&, const Lane& L, const double x0[2], const double x1[2],
+                                        const double x2[2], const double xk[2], double rr[2], double ss[2],
+                                        double tt[2], double ms[2]) const {
+    const int lane = L.g * 4 + L.q;
+    double v0[F::kNF], v1[F::kNF];
+#pragma unroll
+    for (int c = 0; c < F::kNF; ++c) {
+      const double2 p = fac[K][c][lane];
+      v0[c] = p.x;
+      v1[c] = p.y;
+    }
+    F::apply(v0, x0[0], x1[0], x2[0], xk[0], rr[0], ss[0], tt[0], ms[0]);
+    F::apply(v1, x0[1], x1[1], x2[1], xk[1], rr[1], ss[1], tt[1], ms[1]);
+  }
 };
 
 // Parallelepiped: g = w (x) h (geometry.py:389-398), w_j w_i per fibre, w_k folded.
 template <bool HELM>
 struct Ppd {
-  static constexpr bool kTri = false, kWFold = true, kGather = false;
+  static constexpr bool kTri = false, kWFold = true, kGather = false, kFields = HELM;
   double h[7], wji[2];
   const double* lam0;
   const double* lam1;
@@ -340,9 +424,8 @@ struct Ppd {
   __device__ __forceinline__ void prepare(const hx_axlocal_args& a, ElemGeo&, const Lane& L) {
 #pragma unroll
     for (int c = 0; c < 7; ++c) h[c] = __ldg(a.h + L.e * 7 + c);
-    const double wj = fast::wr(L.g);
-    wji[0] = wj * fast::wr(2 * L.q);
-    wji[1] = wj * fast::wr(2 * L.q + 1);
+    wji[0] = g_W8[L.g] * g_W8[2 * L.q];
+    wji[1] = g_W8[L.g] * g_W8[2 * L.q + 1];
     if (HELM) {
       lam0 = a.lam0 ? a.lam0 + L.e * N3 : nullptr;
       lam1 = a.lam1 ? a.lam1 + L.e * N3 : nullptr;
@@ -375,7 +458,7 @@ struct Ppd {
 // Stored (Nek-style) factors: 6 (+gwj) SoA loads per node (axlocal.py:181-185).
 template <bool HELM>
 struct Stored {
-  static constexpr bool kTri = false, kWFold = false, kGather = false;
+  static constexpr bool kTri = false, kWFold = false, kGather = false, kFields = HELM;
   const double* gp;
   const double* gwj;
   const double* lam0;
@@ -423,6 +506,9 @@ struct Stored {
   }
 };
 
+#ifndef HX_MMA3_NREG
+#define HX_MMA3_NREG 168  // ax8m3: 4 CTAs (12 warps) / SM; 150 vs 145 GDOF/s at 128 (profiles/r02_mma_c3_ab.txt)
+#endif
 #ifndef HX_MMA_AHEAD_WAVES4
 #define HX_MMA_AHEAD_WAVES4 5  // L2 prefetch distance in quarter waves of resident warps
 #endif
@@ -488,44 +574,86 @@ struct XSrc {
 };
 
 // One column of one element: x -> y, with the geometry prepared.
-template <typename F, int NCOL, bool GATHER = false, bool CGP = false>
-__device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, const F& fac, const Lane& L,
-                                       const double Dr[2], const double Ds[2], const double Dt[2],
+// xa / xb: the thread's two k-fibres of x, loaded by the caller before the
+// geometry prologue so that their latency hides behind it.
+template <typename F, int NCOL, bool GATHER, bool CGP>
+__device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, double (*tiles)[64], const F& fac,
+                                       const Lane& L, const XSrc<NCOL, GATHER, CGP>& X, double xa[8],
+                                       double xb[8], const double Dr[2], const double Ds[2], const double Dt[2],
                                        const double Dy[2], int col) {
   const int g = L.g, q = L.q;
-  const XSrc<NCOL, GATHER, CGP> X(a, L, col);
-  double xa[8], xb[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) X.pair(k, g, 2 * q, xa[k], xb[k]);
   double ta[8], tb[8];
   fast::eo8<0>(xa, ta);
   fast::eo8<0>(xb, tb);
 
-#define HX_SLICE(K)                                                                                    \
-  {                                                                                                    \
-    double x0[2], x1[2], x2[2] = {ta[K], tb[K]}, xk[2] = {xa[K], xb[K]};                               \
-    dmma(x0[0], x0[1], xa[K], Dr[0], 0.0, 0.0);                                                        \
-    dmma(x0[0], x0[1], xb[K], Dr[1], x0[0], x0[1]);                                                    \
-    const double bx0 = X.at(K, q, g), bx1 = X.at(K, q + 4, g);                                          \
-    dmma(x1[0], x1[1], Ds[0], bx0, 0.0, 0.0);                                                          \
-    dmma(x1[0], x1[1], Ds[1], bx1, x1[0], x1[1]);                                                      \
-    double rr[2], ss[2], tt[2], ms[2] = {0.0, 0.0};                                                    \
-    fac.template slice<K>(S, L, x0, x1, x2, xk, rr, ss, tt, ms);                                       \
-    ta[K] = tt[0];                                                                                     \
-    tb[K] = tt[1];                                                                                     \
-    double* tl = S.tile[K & 1];                                                                        \
-    *reinterpret_cast<double2*>(tl + g * 8 + 2 * q) = make_double2(ss[0], ss[1]);                      \
-    __syncwarp();                                                                                      \
-    double y0, y1;                                                                                     \
-    dmma(y0, y1, rr[0], Dt[0], ms[0], ms[1]);                                                          \
-    dmma(y0, y1, rr[1], Dt[1], y0, y1);                                                                \
-    dmma(y0, y1, Dy[0], tl[q * 8 + g], y0, y1);                                                        \
-    dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);                                                  \
-    xa[K] = y0;                                                                                        \
-    xb[K] = y1;                                                                                        \
+#ifndef HX_MMA_YR_FIRST  // D_s^T ss first: +1 % over D_r^T rr first (profiles/r02_mma_sched_ab.txt)
+#define HX_MMA_Y(K)                                          \
+  dmma(y0, y1, Dy[0], tl[q * 8 + g], ms[0], ms[1]);          \
+  dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);          \
+  dmma(y0, y1, rr[0], Dt[0], y0, y1);                        \
+  dmma(y0, y1, rr[1], Dt[1], y0, y1);
+#else
+#define HX_MMA_Y(K)                                          \
+  dmma(y0, y1, rr[0], Dt[0], ms[0], ms[1]);                  \
+  dmma(y0, y1, rr[1], Dt[1], y0, y1);                        \
+  dmma(y0, y1, Dy[0], tl[q * 8 + g], y0, y1);                \
+  dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);
+#endif
+  // forward r / s derivatives of slice K (two chained DMMAs each)
+#define HX_FWD(K, X0, X1)                                               \
+  double X0[2], X1[2];                                                  \
+  {                                                                     \
+    dmma(X0[0], X0[1], xa[K], Dr[0], 0.0, 0.0);                         \
+    dmma(X0[0], X0[1], xb[K], Dr[1], X0[0], X0[1]);                     \
+    const double bx0 = X.at(K, q, g), bx1 = X.at(K, q + 4, g);          \
+    dmma(X1[0], X1[1], Ds[0], bx0, 0.0, 0.0);                           \
+    dmma(X1[0], X1[1], Ds[1], bx1, X1[0], X1[1]);                       \
   }
-  HX_SLICE(0) HX_SLICE(1) HX_SLICE(2) HX_SLICE(3) HX_SLICE(4) HX_SLICE(5) HX_SLICE(6) HX_SLICE(7)
+  // node stage and transposed r / s of slice K, from its forward derivatives
+#define HX_BWD(K, X0, X1)                                                                \
+  {                                                                                      \
+    double x2[2] = {ta[K], tb[K]}, xk[2] = {xa[K], xb[K]};                               \
+    double rr[2], ss[2], tt[2], ms[2] = {0.0, 0.0};                                      \
+    fac.template slice<K>(S, L, X0, X1, x2, xk, rr, ss, tt, ms);                         \
+    ta[K] = tt[0];                                                                       \
+    tb[K] = tt[1];                                                                       \
+    double* tl = tiles[K & 1];                                                           \
+    *reinterpret_cast<double2*>(tl + g * 8 + 2 * q) = make_double2(ss[0], ss[1]);        \
+    __syncwarp();                                                                        \
+    double y0, y1;                                                                       \
+    HX_MMA_Y(K)                                                                          \
+    xa[K] = y0;                                                                          \
+    xb[K] = y1;                                                                          \
+  }
+#if !defined(HX_MMA_NO_PIPE) && !defined(HX_MMA_PIPE2)
+  // software pipeline (+2 % with Ys first, profiles/r02_mma_sched_ab.txt): slice K+1's forward DMMAs are issued ahead of slice K's node stage
+  HX_FWD(0, f0a, f0b)
+  HX_FWD(1, f1a, f1b) HX_BWD(0, f0a, f0b)
+  HX_FWD(2, f2a, f2b) HX_BWD(1, f1a, f1b)
+  HX_FWD(3, f3a, f3b) HX_BWD(2, f2a, f2b)
+  HX_FWD(4, f4a, f4b) HX_BWD(3, f3a, f3b)
+  HX_FWD(5, f5a, f5b) HX_BWD(4, f4a, f4b)
+  HX_FWD(6, f6a, f6b) HX_BWD(5, f5a, f5b)
+  HX_FWD(7, f7a, f7b) HX_BWD(6, f6a, f6b)
+  HX_BWD(7, f7a, f7b)
+#elif defined(HX_MMA_PIPE2)
+  HX_FWD(0, f0a, f0b) HX_FWD(1, f1a, f1b)
+  HX_FWD(2, f2a, f2b) HX_BWD(0, f0a, f0b)
+  HX_FWD(3, f3a, f3b) HX_BWD(1, f1a, f1b)
+  HX_FWD(4, f4a, f4b) HX_BWD(2, f2a, f2b)
+  HX_FWD(5, f5a, f5b) HX_BWD(3, f3a, f3b)
+  HX_FWD(6, f6a, f6b) HX_BWD(4, f4a, f4b)
+  HX_FWD(7, f7a, f7b) HX_BWD(5, f5a, f5b)
+  HX_BWD(6, f6a, f6b) HX_BWD(7, f7a, f7b)
+#else
+#define HX_SLICE(K, A, B) { HX_FWD(K, A, B) HX_BWD(K, A, B) }
+  HX_SLICE(0, f0a, f0b) HX_SLICE(1, f1a, f1b) HX_SLICE(2, f2a, f2b) HX_SLICE(3, f3a, f3b)
+  HX_SLICE(4, f4a, f4b) HX_SLICE(5, f5a, f5b) HX_SLICE(6, f6a, f6b) HX_SLICE(7, f7a, f7b)
 #undef HX_SLICE
+#endif
+#undef HX_FWD
+#undef HX_BWD
+#undef HX_MMA_Y
 
   double ya[8], yb[8];
   if (F::kWFold) {
@@ -557,8 +685,10 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, con
   }
 }
 
-template <typename F, int NCOL, int MINB, bool GATHER = false, bool CGP = false>
-__global__ void __launch_bounds__(32, MINB) ax8m(const __grid_constant__ hx_axlocal_args a) {
+// NREG: register cap (__maxnreg__); 65536 / (32 NREG) warps per SM are resident
+template <typename F, int NCOL, int NREG, bool GATHER = false, bool CGP = false>
+__global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a) {
+  constexpr int MINB = 65536 / (32 * NREG);
   __shared__ ElemGeo S;
   const int lane = threadIdx.x;
   // n_col = 3: one warp per (element, column), each the n_col = 1 arithmetic
@@ -576,7 +706,7 @@ __global__ void __launch_bounds__(32, MINB) ax8m(const __grid_constant__ hx_axlo
       if (lane == 0) {
         if (!GATHER) bulk_prefetch_l2(a.x + ahead * N3 * NCOL, 4096u * NCOL);
         if (F::kTri) bulk_prefetch_l2(a.verts + ahead * 24, 192u);
-      } else {
+      } else if (F::kFields) {
         if (a.lam_geo) bulk_prefetch_l2(a.lam_geo + ahead * N3, 4096u);
         if (a.lam2) bulk_prefetch_l2(a.lam2 + ahead * N3, 4096u);
         if (a.lam3) bulk_prefetch_l2(a.lam3 + ahead * N3, 4096u);
@@ -600,6 +730,10 @@ __global__ void __launch_bounds__(32, MINB) ax8m(const __grid_constant__ hx_axlo
       }
     }
   }
+  const XSrc<NCOL, GATHER, CGP> X(a, L, col);
+  double xa[8], xb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
   double Dr[2], Ds[2], Dt[2], Dy[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
@@ -618,26 +752,134 @@ __global__ void __launch_bounds__(32, MINB) ax8m(const __grid_constant__ hx_axlo
   F fac;
   fac.prepare(a, S, L);
   if (F::kTri) __syncwarp();
-  column<F, NCOL, GATHER, CGP>(a, S, fac, L, Dr, Ds, Dt, Dy, col);
+  column<F, NCOL, GATHER, CGP>(a, S, S.tile, fac, L, X, xa, xb, Dr, Ds, Dt, Dy, col);
 }
 
-template <typename F, int MINB = 12>
+// n_col = 3 with factor reuse, trilinear sources: one CTA of three warps per
+// element, warp c owning column c.  Stage A by the whole CTA; then warps 0 / 1
+// prepare fibre b = 0 / 1 of their lanes and evaluate its per-node factors
+// (adj(K), scale[, mass coefficient]) for all eight slices into shared memory
+// while warp 2 fills the K00 / K11 tables; then every warp runs the n_col = 1
+// column pass with the factors read back (FacLoaded), so each column is
+// bitwise an n_col = 1 apply (the factors are the same roundings, stored).
+template <typename F, int NREG>
+__global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args a) {
+  constexpr int MINB = 65536 / (32 * NREG);
+  __shared__ ElemGeo S;
+  __shared__ double s_tile[2][2][64];  // warps 1, 2 (warp 0 uses S.tile)
+  __shared__ double2 s_fac[8][F::kNF][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Lane L;
+  L.e = blockIdx.x;
+  L.g = lane >> 2;
+  L.q = lane & 3;
+  if (threadIdx.x < 2) {
+    const int64_t ahead = L.e + (int64_t)148 * MINB * HX_MMA_AHEAD_WAVES4 / 4 / 3;
+    if (ahead < a.n_elements) {
+      if (threadIdx.x == 0) {
+        bulk_prefetch_l2(a.x + ahead * N3 * 3, 4096u * 3);
+        bulk_prefetch_l2(a.verts + ahead * 24, 192u);
+      } else {
+        if (a.lam_geo) bulk_prefetch_l2(a.lam_geo + ahead * N3, 4096u);
+        if (a.lam2) bulk_prefetch_l2(a.lam2 + ahead * N3, 4096u);
+        if (a.lam3) bulk_prefetch_l2(a.lam3 + ahead * N3, 4096u);
+        if (a.lam0) bulk_prefetch_l2(a.lam0 + ahead * N3, 4096u);
+        if (a.lam1) bulk_prefetch_l2(a.lam1 + ahead * N3, 4096u);
+      }
+    }
+  }
+  const XSrc<3, false, false> X(a, L, w);
+  double xa[8], xb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
+  double Dr[2], Ds[2], Dt[2], Dy[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    Dr[s] = g_D8[L.g * 8 + 2 * L.q + s];
+    Ds[s] = g_D8[L.g * 8 + L.q + 4 * s];
+    Dt[s] = g_D8[(2 * L.q + s) * 8 + L.g];
+    Dy[s] = g_D8[(L.q + 4 * s) * 8 + L.g];
+  }
+  stage_a(threadIdx.x, a.verts + L.e * 24, S);
+  __syncthreads();
+  {
+    F fac;
+#ifdef HX_MMA3_FIBRE_SPLIT  // warps 0 / 1 one fibre each, all slices (A/B: -3 %)
+    if (w < 2) {
+      fac.prepare_one(a, S, L, w);
+    } else {
+      tri_tables(S, lane & 7, lane >> 3);
+      tri_tables(S, lane & 7, 4 + (lane >> 3));
+    }
+    __syncthreads();
+    if (w < 2) {
+      double* dst = reinterpret_cast<double*>(&s_fac[0][0][lane]) + w;
+#define HX_FAC(K)                                                        \
+  {                                                                      \
+    double v[F::kNF];                                                    \
+    fac.template node_factors<K>(S, L, w, v);                            \
+    _Pragma("unroll") for (int c = 0; c < F::kNF; ++c) dst[((K)*F::kNF + c) * 64] = v[c]; \
+  }
+      HX_FAC(0) HX_FAC(1) HX_FAC(2) HX_FAC(3) HX_FAC(4) HX_FAC(5) HX_FAC(6) HX_FAC(7)
+#undef HX_FAC
+    }
+#else
+    // warps 0 / 1: both fibres of the lane, slices 0-3 / 4-7 (double2 stores)
+    if (w < 2) {
+      fac.prepare_one(a, S, L, 0);
+      fac.prepare_one(a, S, L, 1);
+    } else {
+      tri_tables(S, lane & 7, lane >> 3);
+      tri_tables(S, lane & 7, 4 + (lane >> 3));
+    }
+    __syncthreads();
+#define HX_FAC(K)                                                        \
+  {                                                                      \
+    double v0[F::kNF], v1[F::kNF];                                       \
+    fac.template node_factors<K>(S, L, 0, v0);                           \
+    fac.template node_factors<K>(S, L, 1, v1);                           \
+    _Pragma("unroll") for (int c = 0; c < F::kNF; ++c) s_fac[K][c][lane] = make_double2(v0[c], v1[c]); \
+  }
+    if (w == 0) {
+      HX_FAC(0) HX_FAC(1) HX_FAC(2) HX_FAC(3)
+    } else if (w == 1) {
+      HX_FAC(4) HX_FAC(5) HX_FAC(6) HX_FAC(7)
+    }
+#undef HX_FAC
+#endif
+  }
+  __syncthreads();
+  FacLoaded<F> fl;
+  fl.fac = s_fac;
+  // each warp transposes through its own tile pair
+  column<FacLoaded<F>, 3, false, false>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy,
+                                        w);
+}
+
+template <typename F, int NREG = 168>
 cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements * a.n_col > 0x7fffffffLL) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)(a.n_elements * a.n_col);
   if (a.gather) {  // n_col = 1 (checked by hx_axlocal)
     if constexpr (F::kGather) {
       if (a.cg_r)
-        ax8m<F, 1, MINB, true, true><<<grid, 32, 0, s>>>(a);
+        ax8m<F, 1, NREG, true, true><<<grid, 32, 0, s>>>(a);
       else
-        ax8m<F, 1, MINB, true><<<grid, 32, 0, s>>>(a);
+        ax8m<F, 1, NREG, true><<<grid, 32, 0, s>>>(a);
     } else {
       return cudaErrorNotSupported;
     }
-  } else if (a.n_col == 3)
-    ax8m<F, 3, MINB><<<grid, 32, 0, s>>>(a);
+  } else if (a.n_col == 3) {
+    if constexpr (F::kTri) {
+      if (a.reserved != 71) {  // 71: the per-column warps without factor reuse (A/B)
+        ax8m3<F, HX_MMA3_NREG><<<(unsigned)a.n_elements, 96, 0, s>>>(a);
+        return cudaGetLastError();
+      }
+    }
+    ax8m<F, 3, NREG><<<grid, 32, 0, s>>>(a);
+  }
   else
-    ax8m<F, 1, MINB><<<grid, 32, 0, s>>>(a);
+    ax8m<F, 1, NREG><<<grid, 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -657,7 +899,13 @@ extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
     return cudaErrorNotSupported;  // the lattice gather is built for the trilinear Poisson sources
   switch (a->factor_source) {
     case HX_TRILINEAR:
-      return helm ? launch<Tri<true>>(*a, s) : launch<Tri<false>>(*a, s);
+      if (helm) return launch<Tri<true>>(*a, s);
+      switch (a->reserved) {  // register-cap A/B (tools/kernel_ab.py)
+        case 61: return launch<Tri<false>, 160>(*a, s);
+        case 62: return launch<Tri<false>, 152>(*a, s);
+        case 63: return launch<Tri<false>, 144>(*a, s);
+        default: return launch<Tri<false>>(*a, s);
+      }
     case HX_TRILINEAR_PARTIAL:
       return launch<TriStoredScale<false>>(*a, s);
     case HX_TRILINEAR_MERGED:
@@ -684,7 +932,9 @@ extern "C" cudaError_t hx_upload_basis_mma(int n1, const double* pts, const doub
     }
   for (int m = 0; m < 8; ++m) iw[m] = 1.0 / w[m];
   err = cudaMemcpyToSymbol(hx::mma::c_EOW, eow, sizeof(eow));
-  if (err == cudaSuccess) err = cudaMemcpyToSymbol(hx::mma::c_IW, iw, sizeof(iw));
+  if (err == cudaSuccess) err = cudaMemcpyToSymbol(g_IW8, iw, sizeof(iw));
+  if (err == cudaSuccess) err = cudaMemcpyToSymbol(g_X8, pts, 8 * sizeof(double));
+  if (err == cudaSuccess) err = cudaMemcpyToSymbol(g_W8, w, 8 * sizeof(double));
   if (err != cudaSuccess) return err;
   return cudaMemcpyToSymbol(g_D8, d, 64 * sizeof(double));
 }
