@@ -57,6 +57,13 @@ class World:
             self.pg = dist
         return self
 
+    def host_staged(self, tensor) -> bool:
+        """True when ``tensor`` lives on a GPU but the process group is gloo
+        (no device P2P): communication then goes through host copies."""
+        if not self.pg or not getattr(tensor, "is_cuda", False):
+            return False
+        return self.pg.get_backend() == "gloo"
+
     def barrier(self) -> None:
         if self.pg:
             self.pg.barrier()

@@ -320,21 +320,26 @@ class GlobalOperator:
         dist = w.pg
         L = self.layout
         P = L.plane
+        # NCCL moves device planes directly; gloo has no device P2P, so its planes
+        # are staged through host memory (the CPU-only test / debugging path)
+        stage = w.host_staged(v)
         ops, recv_lo, recv_hi = [], None, None
         if w.rank > 0:
             send_lo = v[:P].contiguous()
+            send_lo = send_lo.cpu() if stage else send_lo
             recv_lo = torch.empty_like(send_lo)
             ops += [dist.P2POp(dist.isend, send_lo, w.rank - 1), dist.P2POp(dist.irecv, recv_lo, w.rank - 1)]
         if w.rank < w.size - 1:
             send_hi = v[-P:].contiguous()
+            send_hi = send_hi.cpu() if stage else send_hi
             recv_hi = torch.empty_like(send_hi)
             ops += [dist.P2POp(dist.isend, send_hi, w.rank + 1), dist.P2POp(dist.irecv, recv_hi, w.rank + 1)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
         if recv_lo is not None:
-            v[:P] = recv_lo + v[:P]  # lower rank's partial first
+            v[:P] = recv_lo.to(v.device) + v[:P]  # lower rank's partial first
         if recv_hi is not None:
-            v[-P:] = v[-P:] + recv_hi
+            v[-P:] = v[-P:] + recv_hi.to(v.device)
 
     def apply_global(self, global_values):
         """Reference form (single process): host (n_global,) or (n_global, n_col) in and out."""
@@ -392,12 +397,14 @@ class _Reducer:
         torch = _torch()
         w = self.op.world
         if w.size > 1:
-            parts = [torch.zeros(1, dtype=torch.float64, device=self.op.device) for _ in range(w.size)]
-            w.pg.all_gather(parts, self.scal[slot:slot + 1].clone())
+            mine = self.scal[slot:slot + 1].clone()
+            dev = "cpu" if w.host_staged(mine) else self.op.device
+            parts = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(w.size)]
+            w.pg.all_gather(parts, mine.to(dev))
             total = parts[0].clone()
             for t in parts[1:]:
-                total = total + t
-            self.scal[slot:slot + 1] = total
+                total = total + t  # rank order: bitwise reproducible for a given rank count
+            self.scal[slot:slot + 1] = total.to(self.op.device)
         return float(self.scal[slot].item())
 
 

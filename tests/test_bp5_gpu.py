@@ -78,7 +78,11 @@ def test_nekbone_matches_reference_golden(golden):
         res, _ = S.nekbone_benchmark(conf)
         for r, want in zip(res, cfg["results"]):
             assert r.variant == want["variant"]
-            assert abs(r.iterations - want["iterations"]) <= 1, (cfg, r)
+            # Table 5 observable: identical iteration counts (exact), and the same
+            # error level (the final iterate's error moves at the 1 % level under
+            # 1e-16 changes of the operator's rounding; the reference's own numpy
+            # builds differ that much)
+            assert r.iterations == want["iterations"], (cfg, r)
             assert r.error == pytest.approx(want["error"], rel=5e-2), (cfg, r)
 
 
