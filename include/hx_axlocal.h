@@ -100,9 +100,13 @@ typedef struct {
   double lam1_value;
   int32_t kernel;         /* 0 = best measured kernel for (order, factor source);
                              1 = slice kernel (paper Algorithm 4, every order);
-                             2 = fast kernel (specialised N=7, else order-generic);
-                             3 = element-per-thread kernel (orders 1, 2 only) */
-  int32_t reserved;
+                             2 = fast kernel (specialised N=7 ax8s / ax8c3, else order-generic);
+                             3 = element-per-thread kernel (orders 1, 2 only);
+                             4 = DMMA kernel (order 7 only: r/s contractions on
+                                 mma.sync m8n8k4 f64, ax_mma.cu) */
+  int32_t reserved;       /* must be 0: nonzero values select experimental kernel
+                             variants for the A/B tools and are rejected
+                             (HX_ERR_INVALID) unless HX_TUNING=1 is set */
   /* Optional fused gather (BP5): when gather != 0, x is NOT element-local but
    * the slab lattice vector of gather_box and each element reads its nodes
    * straight from it (Q u, mesh.py:286-294).  Order 7, n_col 1, and the

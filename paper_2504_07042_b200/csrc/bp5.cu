@@ -254,13 +254,16 @@ __global__ void mask_rows_kernel(Box b, double* __restrict__ v) {
 __global__ void gather_rows_kernel(Box b, const double* __restrict__ u, double* __restrict__ xl) {
   const int n1 = b.order + 1, n3 = n1 * n1 * n1;
   const int nx = b.ex * b.order + 1, ny = b.ey * b.order + 1;
-  const int cy = blockIdx.y % b.ey, cz = blockIdx.y / b.ey;  // element row (cy, cz)
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < b.ex * n3; t += gridDim.x * blockDim.x) {
-    const int cx = t / n3, node = t - cx * n3;
-    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
-    const int64_t e = ((int64_t)cz * b.ey + cy) * b.ex + cx;
-    const int64_t g = ((int64_t)(cz * b.order + k) * ny + cy * b.order + j) * nx + cx * b.order + i;
-    xl[(e * n3 + node) * b.n_col + b.col] = u[g];
+  // element rows (cy, cz) grid-strided over grid.y (<= 65535 rows per launch)
+  for (int rowe = blockIdx.y; rowe < b.ey * b.nz_el; rowe += gridDim.y) {
+    const int cy = rowe % b.ey, cz = rowe / b.ey;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < b.ex * n3; t += gridDim.x * blockDim.x) {
+      const int cx = t / n3, node = t - cx * n3;
+      const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+      const int64_t e = ((int64_t)cz * b.ey + cy) * b.ex + cx;
+      const int64_t g = ((int64_t)(cz * b.order + k) * ny + cy * b.order + j) * nx + cx * b.order + i;
+      xl[(e * n3 + node) * b.n_col + b.col] = u[g];
+    }
   }
 }
 
@@ -360,7 +363,8 @@ dim3 band_grid(const Box& b) {
 extern "C" cudaError_t hx_bp5_gather_impl(Box b, const double* u, double* xl, cudaStream_t s) {
   const int n3 = (b.order + 1) * (b.order + 1) * (b.order + 1);
   const int per_row = b.ex * n3;
-  dim3 grid((per_row + 255) / 256, b.ey * b.nz_el);
+  const int rows = b.ey * b.nz_el;
+  dim3 grid((per_row + 255) / 256, rows < 65535 ? rows : 65535);
   hx::bp5::gather_rows_kernel<<<grid, 256, 0, s>>>(b, u, xl);
   return cudaGetLastError();
 }

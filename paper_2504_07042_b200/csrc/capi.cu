@@ -5,6 +5,8 @@
 // device-side "first bad index" words that the Python layer turns into
 // GeometryError with the reference's messages.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "hx_common.cuh"
@@ -178,9 +180,21 @@ extern "C" int hx_set_basis(int32_t order, const double* points, const double* w
   return cuda_status(cudaDeviceSynchronize(), "hx_set_basis");
 }
 
+// Nonzero hx_axlocal_args.reserved selects experimental kernel variants for the
+// development A/B tools; it is honoured only with HX_TUNING=1 in the environment.
+static bool tuning_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("HX_TUNING");
+    return v && v[0] && strcmp(v, "0") != 0;
+  }();
+  return on;
+}
+
 extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
   g_last_error.clear();
   if (!a) return fail(HX_ERR_INVALID, "null args");
+  if (a->reserved != 0 && !tuning_enabled())
+    return fail(HX_ERR_INVALID, "hx_axlocal_args.reserved must be 0 (tuning hooks need HX_TUNING=1)");
   if (int st = bind_device(a->x)) return st;
   if (!order_ok(a->order)) return fail(HX_ERR_UNSUPPORTED, "order must be in 1..15");
   if (a->n_col != 1 && a->n_col != 3) return fail(HX_ERR_INVALID, "n_col must be 1 or 3");
@@ -260,6 +274,12 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
     cudaError_t e = hx_fast_launch(a, s);  // specialised N = 7
     if (e != cudaErrorNotSupported) return cuda_status(e, "hx_axlocal(fast)");
     (void)cudaGetLastError();
+    // only the N = 7 kernels read the lattice; never fall through to an
+    // element-local kernel with a lattice x (out-of-bounds reads)
+    if (a->gather)
+      return fail(HX_ERR_UNSUPPORTED,
+                  "fused lattice gather: no kernel for this request (the ax8s gather path needs 16-byte "
+                  "aligned x and vertices)");
     // kernel 0 keeps the slice kernel where it measures faster (stored at order 1;
     // the fused-gather path at orders 1-2; profiles/r01_order_sweep.txt)
     const bool tri = a->factor_source == HX_TRILINEAR || a->factor_source == HX_TRILINEAR_PARTIAL ||
@@ -345,6 +365,9 @@ int box_ok(const hx_box* b) {
     return fail(HX_ERR_UNSUPPORTED, "box too large for 32-bit element / lattice indices");
   if ((b->n_col != 1 && b->n_col != 3) || b->col < 0 || b->col >= b->n_col)
     return fail(HX_ERR_INVALID, "bad column selection");
+  // lattice rows / planes of the slab index grid.y / grid.z of the row and band kernels
+  if ((int64_t)b->ey * b->order + 1 > 65535 || (int64_t)b->nz_el * b->order + 1 > 65535)
+    return fail(HX_ERR_UNSUPPORTED, "slab too large: at most 65535 lattice rows along y and planes along z");
   return HX_OK;
 }
 }  // namespace

@@ -408,12 +408,45 @@ class _Reducer:
         return float(self.scal[slot].item())
 
 
-def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mask=True) -> CgReport:
+def _node_mask(op: GlobalOperator, mask):
+    """The reference's ``mask`` argument as (kind, device tensor): kind "none"
+    (None / False: unmasked), "box" (True, or an array equal to the box
+    interior: the kernel-computed mask and the fused CG paths), or "array"
+    (any other boolean node array, True = kept, applied as given)."""
+    torch = _torch()
+    if mask is None or mask is False:
+        return "none", None
+    if mask is True:
+        return "box", None
+    L = op.layout
+    m = mask.to(torch.bool) if isinstance(mask, torch.Tensor) else torch.as_tensor(np.asarray(mask, dtype=bool))
+    if m.ndim != 1:
+        raise ValueError("mask must be a boolean node array (True = kept)")
+    if m.numel() == L.global_node_count and m.numel() != L.n_local:
+        if op.world.size != 1:
+            raise ValueError("a global mask is the single-process form; pass the slab's (n_local,) mask per rank")
+        m = m[L.global_slice()]
+    if m.numel() != L.n_local:
+        raise ValueError("mask length does not match the mesh")
+    m = m.to(op.device)
+    box = torch.ones(L.n_local, dtype=torch.float64, device=op.device)
+    op.backend.mask(L, box)
+    if torch.equal(m, box.to(torch.bool)):
+        return "box", None
+    return "array", m.to(torch.float64)
+
+
+def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mask=None, threads: int = 1) -> CgReport:
     """Unpreconditioned CG on M A M (reference solver.py:124-178), all on the device.
 
     ``b`` is the rank's slab vector (device tensor) or, single process, a host
-    (n_global,) array; ``mask=True`` keeps the box interior (homogeneous
-    Dirichlet), ``mask=None`` solves unmasked.
+    (n_global,) array.  ``mask`` follows the reference: None (the default)
+    solves unmasked; a boolean node array keeps the nodes where it is True (the
+    negated boundary mask gives homogeneous Dirichlet conditions) -- the global
+    (n_global,) array single-process, or the slab's (n_local,) array per rank;
+    ``True`` is shorthand for the box interior.  The box-interior mask runs the
+    fused kernels; any other mask is applied as given.  ``threads`` is accepted
+    and ignored (the reference's thread-pool split has no GPU meaning).
     """
     torch = _torch()
     B, L = op.backend, op.layout
@@ -421,9 +454,17 @@ def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mas
         hb = np.asarray(b, dtype=float)
         b = torch.as_tensor(np.ascontiguousarray(hb.T if hb.ndim == 2 else hb), device=op.device)
     b = b.to(device=op.device, dtype=torch.float64).clone()
-    masked = mask is not None and mask is not False
-    if masked:
-        op.mask(b)
+    kind, marr = _node_mask(op, mask)
+    masked = kind == "box"
+
+    def apply_mask(v):
+        if kind == "box":
+            op.mask(v)
+        elif kind == "array":
+            v.mul_(marr)  # columns broadcast over the last (node) axis
+        return v
+
+    apply_mask(b)
     red = _Reducer(op)
     x = torch.zeros_like(b)
     bb = red.dot(b, b, 0)
@@ -456,8 +497,7 @@ def cg_solve(op: GlobalOperator, b, tol: float = 1e-8, max_iter: int = 1000, mas
             pap = float(red.scal[1].item())
         else:
             op.apply(p, out=ap)
-            if masked:
-                op.mask(ap)
+            apply_mask(ap)
             pap = red.dot(p, ap, 1)
         if not math.isfinite(pap):
             raise FloatingPointError("CG broke down: non-finite curvature")

@@ -124,3 +124,56 @@ def test_fused_p_update_is_bitwise_the_plain_cg():
         fused = S.cg_solve(op, b, tol=1e-10, max_iter=40)
         assert fused.iterations == plain.iterations and fused.residual_history == plain.residual_history
         assert torch.equal(fused.solution, plain.solution)
+
+
+def test_cg_solve_mask_semantics_follow_the_reference():
+    """cg_solve(mask=None) is unmasked, a boolean node array keeps the nodes where
+    it is True (solver.py:124-140), True is the box interior; threads= is accepted."""
+    order, counts = 3, (3, 3, 2)
+    mesh = hx.box_mesh(*counts, order, perturbation=0.1, seed=2)
+    l2g = O.box_l2g(*counts, order)
+    n_global = l2g.max() + 1
+    rng = np.random.default_rng(4)
+    b = rng.standard_normal(n_global)
+    st = O.setup("stored", "helmholtz", order, mesh.vertices, 1.0, 1.0)
+
+    def ref_apply(v):
+        return O.scatter_add(O.apply_setup(st, O.gather(v, l2g)), l2g, n_global)
+
+    op = S.GlobalOperator(mesh, hx.KernelSpec("helmholtz", 1, "stored", order), hx.SpectralBasis.build(order),
+                          lam0=1.0, lam1=1.0)
+    interior = O.interior_mask(*counts, order)
+    custom = interior.copy()
+    custom[rng.choice(np.flatnonzero(interior), size=7, replace=False)] = False
+    for mask in (None, interior, custom):
+        got = S.cg_solve(op, b, tol=1e-10, max_iter=400, mask=mask, threads=4)
+        want_x, want_it, _ = O.cg_solve(ref_apply, b, tol=1e-10, max_iter=400, mask=mask)
+        assert got.converged and got.iterations == want_it, (mask is None, got.iterations, want_it)
+        assert O.rel_diff(got.solution.cpu().numpy(), want_x) <= 1e-9
+    box = S.cg_solve(op, b, tol=1e-10, max_iter=400, mask=True)
+    arr = S.cg_solve(op, b, tol=1e-10, max_iter=400, mask=interior)
+    assert torch.equal(box.solution, arr.solution)  # the interior array takes the kernel mask path
+    with pytest.raises(ValueError):
+        S.cg_solve(op, b, mask=np.ones(5, dtype=bool))
+
+
+def test_fused_gather_misaligned_lattice_view():
+    """A lattice view that is only 8-byte aligned (u[1:]): the DMMA kernel takes it
+    (its lattice loads are 8-byte), the 16-byte ax8s gather path must refuse it
+    with an error instead of falling through to the element-local kernel."""
+    mesh = hx.box_mesh(3, 2, 2, 7, perturbation=0.1, seed=1)
+    L = S.SlabLayout((3, 2, 2), 7)
+    base = torch.randn(L.n_local + 1, dtype=torch.float64, device=DEV)
+    u = base[1:]
+    assert u.data_ptr() % 16 == 8
+    ref = base[1:].clone()
+    xl = torch.empty((L.n_elements, 512, 1), dtype=torch.float64, device=DEV)
+    S.CudaBackend(DEV).gather(L, ref, xl)
+    for src in ("trilinear", "trilinear-partial"):
+        op = hx.LocalOperator(hx.KernelSpec("poisson", 1, src, 7), mesh, hx.SpectralBasis.build(7))
+        y = torch.empty_like(xl)
+        op.apply_lattice_(u, y, L.box())
+        assert torch.equal(y, op.apply(xl)), src
+    op = hx.LocalOperator(hx.KernelSpec("poisson", 1, "stored", 7), mesh, hx.SpectralBasis.build(7))
+    with pytest.raises(ValueError, match="aligned"):
+        op.apply_lattice_(u, torch.empty_like(xl), L.box())

@@ -136,6 +136,11 @@ def test_library_rejects_bad_args_without_gpu():
         _native.check(L.hx_axlocal(ctypes.byref(a), None))
     a = _native.AxArgs(order=7, n_col=1, equation=0, factor_source=1, n_elements=0)
     _native.check(L.hx_axlocal(ctypes.byref(a), None))  # E = 0 is a no-op
+    if os.environ.get("HX_TUNING", "0") in ("", "0"):
+        # the tuning hook field is rejected unless the A/B tools enable it
+        a = _native.AxArgs(order=7, n_col=1, equation=0, factor_source=1, n_elements=4, reserved=3)
+        with pytest.raises(ValueError, match="reserved"):
+            _native.check(L.hx_axlocal(ctypes.byref(a), None))
 
 
 def test_product_does_not_import_oracle():

@@ -6,6 +6,9 @@ Times every (variant, kernel path, tuning hook) at N=7 with CUDA events on a
 resident x/y and prints GDOF/s, TFLOP/s (algorithmic) and HBM GB/s.
 """
 
+import os as _os
+
+_os.environ.setdefault("HX_TUNING", "1")  # the A/B hooks in hx_axlocal_args.reserved
 import argparse
 import time
 import os
