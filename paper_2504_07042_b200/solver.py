@@ -39,7 +39,7 @@ import numpy as np
 from . import _native
 from .axlocal import Equation, FactorSource, KernelSpec, LocalOperator
 from .basis import SpectralBasis
-from .mesh import BoxMesh, box_mesh
+from .mesh import BoxMesh, _kinds_from_defects, box_mesh
 from .sharding import World, slab_layers
 from .workload import ax_flops
 
@@ -616,7 +616,10 @@ def nekbone_benchmark(config: NekboneConfig, world: World | None = None, device=
     basis = SpectralBasis.build(config.order)
     ex, ey, ez = config.elements
     mesh = box_mesh(ex, ey, ez, config.order, perturbation=config.perturbation, seed=config.seed)
-    all_ppd = config.perturbation == 0.0
+    # classify the elements with make_element's defect rule, as the reference does
+    # (solver.py:260), not from the perturbation value (a tiny jitter may stay
+    # within the 1e-12 defect tolerance)
+    all_ppd = bool(_kinds_from_defects(mesh.vertices).all())
     variants = config.variants or compatible_variants(eq, all_ppd)
     variants = tuple(FactorSource(getattr(v, "value", v)) for v in variants)
     variants = tuple(v for v in variants if not (v is FactorSource.PARALLELEPIPED_RECOMPUTE and not all_ppd))
