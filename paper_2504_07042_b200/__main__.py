@@ -1,4 +1,4 @@
-"""``python -m paper_2504_07042_b200 {bench,roofline,nekbone}`` (see cli.py)."""
+"""``python -m paper_2504_07042_b200 roofline ...`` (see cli.py)."""
 import sys
 
 from .cli import main

@@ -1,6 +1,6 @@
-"""The command-line front end (reference cli.py): `roofline` prints the reference's
-bytes for every golden flag combination (tests/golden/roofline_cli.json, written
-by the reference CLI itself); bench CSV round trip; error exit status."""
+"""The command-line front end: `roofline` prints the reference CLI's bytes for
+every golden flag combination (tests/golden/roofline_cli.json, written by the
+reference CLI itself, tests/golden/make_cli_golden.py); error exit status."""
 
 import contextlib
 import io
@@ -45,32 +45,25 @@ def test_roofline_b200_profile():
     assert rows["trilinear"]["m_bytes"] == 8896
 
 
-def test_bench_csv_round_trip():
-    rec = cli.BenchRecord("poisson", 1, 7, "trilinear", 512, 5, 1.5e-5, 1.9e12, 3.4e12, 2.0e13, 95.0)
-    text = cli.bench_records_to_csv([rec, rec])
-    assert cli.parse_bench_csv(text) == [rec, rec]
-    with pytest.raises(ValueError):
-        cli.parse_bench_csv("bad header\n")
-
-
 def test_errors_exit_2(capsys):
     assert cli.main(["roofline", "--profile", "no-such-device"]) == 2
     assert "error:" in capsys.readouterr().err
-    assert cli.main(["bench", "--elements", "4x4"]) == 2
 
 
-@pytest.mark.gpu
-def test_bench_and_nekbone_on_gpu():
-    torch = pytest.importorskip("torch")
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    rc, out = _run(["bench", "--variant", "trilinear", "--elements", "8x8x8", "--perturbation", "0.1",
-                    "--format", "json", "--repeats", "3"])
-    assert rc == 0
-    rec = json.loads(out)
-    assert rec["E"] == 512 and rec["best_time_s"] > 0 and rec["roofline_R_eff"] > 0
-    rc, out = _run(["nekbone", "--elements", "3x3x3", "--order", "5", "--format", "csv", "--variants", "trilinear"])
-    assert rc == 0
-    lines = out.strip().splitlines()
-    assert lines[0] == "variant,iterations,error,wall_time_s,gflops_effective,axlocal_share"
-    assert lines[1].startswith("trilinear,")
+def test_model_api():
+    """The reference's roofline functions behave as documented (roofline.py)."""
+    from paper_2504_07042_b200 import roofline as R
+
+    hw = R.resolve_profile("a100")
+    assert R.machine_balance(hw) == pytest.approx(9.7e12 / 1.360e12)
+    assert hw.peak("matrix") == 19.5e12 and hw.bandwidth("theoretical") == 1.555e12
+    for bad in (lambda: hw.peak("tensor"), lambda: hw.bandwidth("peak"), lambda: R.resolve_profile("k100").peak("matrix"),
+                lambda: R.HardwareProfile("x", 1.0, 2.0, 1.0), lambda: R.KernelModel(1, 1, 1, 5),
+                lambda: R.measured_performance(1, 1, 0.0)):
+        with pytest.raises(ValueError):
+            bad()
+    m = R.KernelModel(100, 50, 10, matrix_unit_flops=60)
+    b_sum, b_max = R.roofline_bounds(m, hw), R.roofline_bounds(m, hw, overlap=True)
+    assert b_sum.t_cmp == pytest.approx(90 / 9.7e12 + 60 / 19.5e12)
+    assert b_max.t_cmp == pytest.approx(max(90 / 9.7e12, 60 / 19.5e12))
+    assert R.measured_performance(10.0, 5.0, 2.0) == (5.0, 7.5)
