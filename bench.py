@@ -17,9 +17,12 @@ streams from HBM; no flush needed).  Timing: W warm-up steps, then K steps
 between CUDA events on the launching stream, barrier + synchronize on both
 sides, max over ranks.  Rank 0 prints one JSON line.
 
---impl reference times the CPU oracle port of the reference algorithm
-(oracle/hosfem_oracle.py, the reference being pure Python/numpy) on a bounded
-element sample with all host threads; rank 0 only.
+--impl reference times the reference's own CPU implementation -- the stock
+``hosfem`` package (LocalOperator.apply with its thread-pool split), installed
+offline into baseline/_ref (git-ignored; it travels with gpurun) -- on a
+bounded element sample of the same workload with all host threads; rank 0
+only.  When baseline/_ref is absent it times the numpy restatement
+(oracle/hosfem_oracle.py, pinned bitwise to the reference), kind "port".
 """
 
 from __future__ import annotations
@@ -136,15 +139,35 @@ class ClockSampler:
             self._stop.set()
             self._t.join()
 
-    def summary(self):
-        if not self.ok:
+    def summary(self, world=None, device=None):
+        """Median SM clock and throttle reasons of the timed region.  With a world
+        of N > 1 ranks (each sampling its own GPU), the reasons are OR-reduced
+        over ranks and the clock is the lowest per-rank median."""
+        med = statistics.median(self.samples) if (self.ok and self.samples) else float("nan")
+        mine = [med, float(self.max_mhz if self.ok else 0), float(len(self.samples)), float(self.reasons)]
+        rows = [mine]
+        if world is not None and world.pg:
+            import torch
+
+            t = torch.tensor(mine, dtype=torch.float64, device=device)
+            parts = [torch.empty_like(t) for _ in range(world.size)]
+            world.pg.all_gather(parts, t)
+            rows = [p.tolist() for p in parts]
+        meds = [r[0] for r in rows if r[0] == r[0]]
+        if not meds:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
-        return {
-            "sm_mhz": statistics.median(self.samples) if self.samples else None,
-            "sm_max_mhz": self.max_mhz,
-            "samples": len(self.samples),
-            "reasons": [n for bit, n in _REASONS.items() if self.reasons & bit and bit != 0x1],
+        bits = 0
+        for r in rows:
+            bits |= int(r[3])
+        out = {
+            "sm_mhz": min(meds),
+            "sm_max_mhz": max(r[1] for r in rows),
+            "samples": int(sum(r[2] for r in rows)),
+            "reasons": [n for bit, n in _REASONS.items() if bits & bit and bit != 0x1],
         }
+        if len(rows) > 1:
+            out["sm_mhz_per_rank"] = [r[0] for r in rows]
+        return out
 
 
 # --------------------------------------------------------------------------
@@ -192,33 +215,78 @@ def peaks():
     return hbm, src, fp64
 
 
-def cpu_sample_baseline(verts, x, sample, budget_s=12.0):
-    """Oracle port (reference algorithm) on the first `sample` elements, all host threads."""
-    from oracle import hosfem_oracle as O
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-    threads = os.cpu_count() or 1
-    v, xs = verts[:sample], x[:sample]
-    st = O.setup("trilinear", "poisson", ORDER, v)
+
+def reference_package():
+    """The stock reference package (hosfem) from baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hosfem")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import hosfem
+    except Exception:  # pragma: no cover - broken install
+        return None
+    return hosfem
+
+
+class CpuAxLocal:
+    """The reference CPU AxLocal on a fixed element sample: the stock hosfem
+    LocalOperator (kind "reference") or, without baseline/_ref, the oracle port
+    (kind "port"); trilinear Poisson N=7, all host threads by default."""
+
+    def __init__(self, verts, x, threads=None):
+        self.threads = threads or os.cpu_count() or 1
+        self.n = len(verts)
+        ref = reference_package()
+        if ref is not None:
+            self.kind = "reference"
+            elements = [ref.make_element(v) for v in verts]
+            spec = ref.KernelSpec(ref.Equation.POISSON, 1, ref.FactorSource.TRILINEAR_RECOMPUTE, ORDER)
+            self._op = ref.LocalOperator(spec, elements, ref.SpectralBasis.build(ORDER))
+            self._x = ref.LocalField(np.asarray(x, dtype=np.float64), ORDER)
+            self.what = "stock hosfem.LocalOperator.apply (baseline/_ref)"
+        else:
+            from oracle import hosfem_oracle as O
+
+            self.kind = "port"
+            self._O = O
+            self._st = O.setup("trilinear", "poisson", ORDER, verts)
+            self._x = np.asarray(x, dtype=np.float64)
+            self.what = "numpy restatement of hosfem LocalOperator.apply (oracle/hosfem_oracle.py)"
+
+    def apply(self, threads=None):
+        t = self.threads if threads is None else threads
+        if self.kind == "reference":
+            return self._op.apply(self._x, threads=t)
+        return self._O.apply_setup(self._st, self._x, threads=t)
+
+    def timed(self, threads=None) -> float:
+        t0 = time.perf_counter()
+        self.apply(threads)
+        return time.perf_counter() - t0
+
+
+def cpu_sample_baseline(verts, x, sample, budget_s=12.0):
+    """The reference CPU path on the first ``sample`` elements of the workload:
+    best of up to 8 applies within ``budget_s`` with all host threads, and the
+    --threads 1 figure on a quarter of the sample."""
+    cpu = CpuAxLocal(verts[:sample], x[:sample])
     best, t_end, reps = float("inf"), time.perf_counter() + budget_s, 0
     while reps < 1 or (time.perf_counter() < t_end and reps < 8):
-        t0 = time.perf_counter()
-        O.apply_setup(st, xs, threads=threads)
-        best = min(best, time.perf_counter() - t0)
+        best = min(best, cpu.timed())
         reps += 1
-    # the reference's --threads 1 figure too (SURVEY 8(d)), on a quarter of the sample
     s1 = max(1, sample // 4)
-    st1 = O.setup("trilinear", "poisson", ORDER, v[:s1])
-    t0 = time.perf_counter()
-    O.apply_setup(st1, xs[:s1], threads=1)
-    t1 = time.perf_counter() - t0
+    t1 = CpuAxLocal(verts[:s1], x[:s1], threads=1).timed()
     dof = sample * (ORDER + 1) ** 3
     return {
         "value": dof / best / 1e9,
         "unit": UNIT,
-        "cores": threads,
-        "kind": "port",
+        "cores": cpu.threads,
+        "kind": cpu.kind,
         "sample": f"{sample} elements of the workload mesh (first elements of the slab), trilinear Poisson N=7, "
-        f"best of {reps} applies, numpy oracle with {threads} threads (element-range split like axlocal.py:245-257)",
+        f"best of {reps} applies, {cpu.what} with {cpu.threads} threads (element-range split, axlocal.py:245-257)",
         "seconds_per_apply": best,
         "value_1thread": s1 * (ORDER + 1) ** 3 / t1 / 1e9,
         "cpu_model": _cpu_model(),
@@ -236,10 +304,28 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+def workload_config(world_size: int, mesh=MESH) -> dict:
+    """The measured workload, identical in both arms' JSON lines."""
+    ex, ey, ez = mesh
+    E_total = ex * ey * ez
+    n3 = (ORDER + 1) ** 3
+    return {
+        "workload": f"box_mesh({ex},{ey},{ez}) N=7 trilinear (pert {PERT}, seed {SEED}), Poisson, n_col=1, "
+        f"{E_total} elements = {E_total * n3 / 1e6:.1f} M DOF, z-slab sharded over {world_size} GPU(s)",
+        "order": ORDER,
+        "elements": E_total,
+        "elements_per_gpu": E_total // world_size,
+        "variant": "trilinear (on-the-fly geometric factors)",
+        "l2": "inputs larger than L2 (x, y 8 B x DOF each per GPU); no flush",
+        "parallelism": f"element-sharded x{world_size}, no data-path collective",
+    }
+
+
 def reference_arm(args, world):
+    """The reference's own CPU AxLocal on this host (rank 0 only): each step
+    applies the operator to a bounded sample of the workload's elements."""
     if world.rank != 0:
         return None
-    from oracle import hosfem_oracle as O
     from paper_2504_07042_b200.mesh import box_mesh
 
     ex, ey, ez = MESH
@@ -248,17 +334,11 @@ def reference_arm(args, world):
     per = ex * ey
     layers = (sample + per - 1) // per
     verts = mesh.vertices_slab(0, layers)[:sample]
-    rng = np.random.default_rng(SEED)
-    x = rng.standard_normal((sample, (ORDER + 1) ** 3, 1))
-    threads = os.cpu_count() or 1
-    st = O.setup("trilinear", "poisson", ORDER, verts)
+    x = np.random.default_rng(SEED).standard_normal((sample, (ORDER + 1) ** 3, 1))
+    cpu = CpuAxLocal(verts, x)
     for _ in range(args.warmup):
-        O.apply_setup(st, x, threads=threads)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.apply_setup(st, x, threads=threads)
-        times.append(time.perf_counter() - t0)
+        cpu.apply()
+    times = [cpu.timed() for _ in range(args.steps)]
     ms = 1e3 * sum(times) / len(times)
     value = sample * (ORDER + 1) ** 3 / (ms * 1e-3) / 1e9
     return {
@@ -275,20 +355,14 @@ def reference_arm(args, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": f"box_mesh{MESH} N=7 trilinear (pert {PERT}, seed {SEED}) Poisson n_col=1; "
-            f"each step a {sample}-element sample on the host",
-            "order": ORDER,
-            "elements_per_step": sample,
-        },
+        "config": workload_config(args.gpus),
         "cpu_baseline": {
             "value": value,
             "unit": UNIT,
-            "cores": threads,
-            "kind": "port",
-            "sample": f"{sample} elements per step, numpy restatement of hosfem LocalOperator.apply "
-            f"(oracle/hosfem_oracle.py) with {threads} threads; the reference is pure Python/numpy "
-            "and cannot travel to the GPU box",
+            "cores": cpu.threads,
+            "kind": cpu.kind,
+            "sample": f"each step: {sample} elements of the workload mesh (first z-layers), {cpu.what} "
+            f"with {cpu.threads} threads; GDOF/s of the sample (elements are independent)",
             "cpu_model": _cpu_model(),
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -339,7 +413,7 @@ def hx_arm(args, world):
             "op": op,
         }
         if clocks is not None:
-            out["clocks"] = clocks.summary()
+            out["clocks"] = clocks.summary(world, dev)
         return out
 
     main = measure("trilinear", with_clocks=True)
@@ -357,16 +431,7 @@ def hx_arm(args, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": f"box_mesh({ex},{ey},{ez}) N=7 trilinear (pert {PERT}, seed {SEED}), Poisson, n_col=1, "
-            f"{E_total} elements = {E_total * n3 / 1e6:.1f} M DOF, z-slab sharded over {world.size} GPU(s)",
-            "order": ORDER,
-            "elements": E_total,
-            "elements_per_gpu": E,
-            "variant": "trilinear (on-the-fly geometric factors)",
-            "l2": "inputs larger than L2 (x, y 8 B x DOF each per GPU); no flush",
-            "parallelism": f"element-sharded x{world.size}, no data-path collective",
-        },
+        "config": dict(workload_config(world.size, (ex, ey, ez)), elements_per_gpu=E),
         "roofline": {
             "bound": "tensor",
             "pipe": "fp64 (DFMA and DMMA share one pipe on B200; tcgen05 has no f64)",
@@ -401,11 +466,11 @@ def hx_arm(args, world):
         result["speedup_vs_in_run_stored"] = main["gdofs"] / variants["stored"]["value"]
     if not args.no_e2e:
         result["e2e"] = e2e(main["op"], x, world, dev, args, E_total, n3)
-    if world.rank == 0 and world.size == 1 and not args.no_cpu_baseline:
-        host_x = x[: args.cpu_sample].cpu().numpy()
-        host_v = verts[: args.cpu_sample].cpu().numpy()
+    host_x = x[: args.cpu_sample].cpu().numpy()
+    host_v = verts[: args.cpu_sample].cpu().numpy()
+    world.close()  # the CPU baseline below is rank 0's host work only (every N)
+    if world.rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_sample_baseline(host_v, host_x, args.cpu_sample)
-    world.close()
     return result if world.rank == 0 else None
 
 

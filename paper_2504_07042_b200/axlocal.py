@@ -75,6 +75,16 @@ def _coerce_enum(cls, value):
     return cls(getattr(value, "value", value))
 
 
+def _as_spec(spec):
+    """This package's KernelSpec from ours, the reference's (same fields, its own
+    enums) or a (equation, n_col, factor_source, order) tuple."""
+    if isinstance(spec, KernelSpec):
+        return spec
+    if isinstance(spec, tuple):
+        return KernelSpec(*spec)
+    return KernelSpec(spec.equation, spec.n_col, spec.factor_source, spec.order)
+
+
 @dataclass(frozen=True)
 class KernelSpec:
     """What to apply: equation, columns, factor variant, order (axlocal.py:58-85)."""
@@ -145,6 +155,7 @@ class LocalOperator:
 
     def __init__(self, spec: KernelSpec, elements, basis, lam0=None, lam1=None, device=None):
         torch = _torch()
+        spec = _as_spec(spec)
         if not torch.cuda.is_available():
             raise RuntimeError("LocalOperator needs a CUDA device (B200); there is no CPU fallback")
         if basis.order != spec.order:
@@ -454,7 +465,7 @@ def dense_local_matrix(spec, element, basis, lam0=None, lam1=None):
     Returns a host numpy array.
     """
     torch = _torch()
-    spec = spec if isinstance(spec, KernelSpec) else KernelSpec(*spec)
+    spec = _as_spec(spec)
     helm = spec.equation is Equation.HELMHOLTZ
     if not helm and (lam0 is not None or lam1 is not None):
         raise ValueError("coefficient fields apply to the Helmholtz operator only")

@@ -21,10 +21,20 @@ def _run(args, timeout=600):
     return json.loads(lines[0])
 
 
+REF_INSTALLED = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "hosfem"))
+
+
 def test_reference_arm_contract():
     d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--cpu-sample", "32"])
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the stock reference package when baseline/_ref holds it, else the pinned port
+    assert d["cpu_baseline"]["kind"] == ("reference" if REF_INSTALLED else "port")
+    assert d["cpu_baseline"]["cores"] >= 1
+    # both arms describe the same workload (the driver compares configs)
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert d["config"] == bench.workload_config(1)
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["gpu_launches"] == 0 and d["value"] > 0
 
@@ -41,7 +51,7 @@ def test_hx_arm_contract():
     assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] < 1.2 and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     c = d["cpu_baseline"]
-    assert c["kind"] == "port" and c["value"] > 0 and c["cores"] >= 1
+    assert c["kind"] == ("reference" if REF_INSTALLED else "port") and c["value"] > 0 and c["cores"] >= 1
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
     assert d["gpu_launches"] == d["steps"]

@@ -149,3 +149,36 @@ def test_product_does_not_import_oracle():
         for f in files:
             if f.endswith(".py"):
                 assert "oracle" not in open(os.path.join(root, f)).read().replace("no oracle", ""), f
+
+
+def test_compat_patch_rebinds_reference_entry_points():
+    """compat.patch_hosfem swaps hosfem's AxLocal names in every loaded module and restores them."""
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "hosfem")):
+        pytest.skip("reference not installed in baseline/_ref")
+    import sys
+
+    sys.path.insert(0, ref)
+    try:
+        import hosfem
+        import hosfem.solver
+
+        from paper_2504_07042_b200.compat import patch_hosfem
+
+        orig = hosfem.axlocal.LocalOperator
+        restore = patch_hosfem(hosfem)
+        assert hosfem.axlocal.LocalOperator is hx.LocalOperator
+        assert hosfem.solver.LocalOperator is hx.LocalOperator
+        assert hosfem.LocalOperator is hx.LocalOperator
+        assert hosfem.axlocal.dense_local_matrix is hx.dense_local_matrix
+        restore()
+        assert hosfem.axlocal.LocalOperator is orig and hosfem.solver.LocalOperator is orig
+        # the reference's own spec objects are accepted as they are
+        spec = hosfem.KernelSpec(hosfem.Equation.HELMHOLTZ, 3, hosfem.FactorSource.TRILINEAR_MERGED, 4)
+        from paper_2504_07042_b200.axlocal import _as_spec
+
+        ours = _as_spec(spec)
+        assert (ours.equation.value, ours.n_col, ours.factor_source.value, ours.order) == ("helmholtz", 3,
+                                                                                           "trilinear-merged", 4)
+    finally:
+        sys.path.remove(ref)
