@@ -174,3 +174,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 }  // namespace hx
+
+// ---------------------------------------------------------------------------
+// Race-detection build (-DHX_PERTURB, tools/race_perturb.sh).  compute-sanitizer
+// is not available on the GPU pool, so shared-memory races are hunted by timing
+// perturbation instead: every barrier first stalls the calling thread for a
+// pseudo-random 0..4095 ns (different per thread, CTA, call and run), so that
+// any shared access not ordered by a barrier interleaves differently from the
+// normal build; the outputs of both builds are then compared bit for bit.
+#ifdef HX_PERTURB
+__device__ __forceinline__ void hx_dbg_jitter(unsigned site) {
+  unsigned h = (threadIdx.x + 97u * threadIdx.y) * 2654435761u;
+  h ^= (blockIdx.x * 40503u + blockIdx.y * 9176u) ^ (site * 2246822519u) ^ (unsigned)clock();
+  h ^= h >> 15;
+  h *= 2246822519u;
+  h ^= h >> 13;
+  __nanosleep(h & 4095u);
+}
+__device__ __forceinline__ void hx_dbg_syncthreads() {
+  hx_dbg_jitter(1);
+  __syncthreads();
+  hx_dbg_jitter(2);
+}
+__device__ __forceinline__ void hx_dbg_syncwarp() {
+  hx_dbg_jitter(3);
+  __syncwarp();
+  hx_dbg_jitter(4);
+}
+#define __syncthreads() hx_dbg_syncthreads()
+#define __syncwarp() hx_dbg_syncwarp()
+#endif
