@@ -586,7 +586,7 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
   fast::eo8<0>(xa, ta);
   fast::eo8<0>(xb, tb);
 
-#ifndef HX_MMA_YR_FIRST  // D_s^T ss first: +1 % over D_r^T rr first (profiles/r02_mma_sched_ab.txt)
+#if !defined(HX_MMA_YR_FIRST)  // D_s^T ss first: +1 % over D_r^T rr first (profiles/r02_mma_sched_ab.txt)
 #define HX_MMA_Y(K)                                          \
   dmma(y0, y1, Dy[0], tl[q * 8 + g], ms[0], ms[1]);          \
   dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);          \
