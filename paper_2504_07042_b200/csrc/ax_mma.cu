@@ -856,7 +856,10 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
                                         w);
 }
 
-template <typename F, int NREG = 168>
+#ifndef HX_MMA_NREG
+#define HX_MMA_NREG 168
+#endif
+template <typename F, int NREG = HX_MMA_NREG>
 cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
   if (a.n_elements * a.n_col > 0x7fffffffLL) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)(a.n_elements * a.n_col);
