@@ -574,18 +574,9 @@ struct XSrc {
 };
 
 // One column of one element: x -> y, with the geometry prepared.
-// xa / xb: the thread's two k-fibres of x, loaded by the caller before the
-// geometry prologue so that their latency hides behind it.
-template <typename F, int NCOL, bool GATHER, bool CGP>
-__device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, double (*tiles)[64], const F& fac,
-                                       const Lane& L, const XSrc<NCOL, GATHER, CGP>& X, double xa[8],
-                                       double xb[8], const double Dr[2], const double Ds[2], const double Dt[2],
-                                       const double Dy[2], int col) {
-  const int g = L.g, q = L.q;
-  double ta[8], tb[8];
-  fast::eo8<0>(xa, ta);
-  fast::eo8<0>(xb, tb);
-
+// The transposed r / s products of a slice, accumulated into (y0, y1) from
+// the mass term ms: one order for every kernel built from these templates
+// (the bitwise n_col contract).
 #if !defined(HX_MMA_YR_FIRST)  // D_s^T ss first: +1 % over D_r^T rr first (profiles/r02_mma_sched_ab.txt)
 #define HX_MMA_Y(K)                                          \
   dmma(y0, y1, Dy[0], tl[q * 8 + g], ms[0], ms[1]);          \
@@ -599,6 +590,20 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
   dmma(y0, y1, Dy[0], tl[q * 8 + g], y0, y1);                \
   dmma(y0, y1, Dy[1], tl[(q + 4) * 8 + g], y0, y1);
 #endif
+
+// xa / xb: the thread's two k-fibres of x, loaded by the caller before the
+// geometry prologue so that their latency hides behind it.
+template <typename F, int NCOL, bool GATHER, bool CGP>
+__device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, double (*tiles)[64], const F& fac,
+                                       const Lane& L, const XSrc<NCOL, GATHER, CGP>& X, double xa[8],
+                                       double xb[8], const double Dr[2], const double Ds[2], const double Dt[2],
+                                       const double Dy[2], int col) {
+  const int g = L.g, q = L.q;
+  double ta[8], tb[8];
+  fast::eo8<0>(xa, ta);
+  fast::eo8<0>(xb, tb);
+
+
   // forward r / s derivatives of slice K (two chained DMMAs each)
 #define HX_FWD(K, X0, X1)                                               \
   double X0[2], X1[2];                                                  \
@@ -653,7 +658,6 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
 #endif
 #undef HX_FWD
 #undef HX_BWD
-#undef HX_MMA_Y
 
   double ya[8], yb[8];
   if (F::kWFold) {
@@ -855,6 +859,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
   column<FacLoaded<F>, 3, false, false>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy,
                                         w);
 }
+
 
 #ifndef HX_MMA_NREG
 #define HX_MMA_NREG 168
