@@ -11,7 +11,8 @@ FAST_ORDERS := 2 3 4 5 6 7 9 10 11 12 13 14 15 16
 GEN_OBJS  := $(foreach n,$(ORDERS),$(OBJ)/ax_generic_$(n).o)
 FASTN_OBJS := $(foreach n,$(FAST_ORDERS),$(OBJ)/ax_fastn_$(n).o)
 LOW_OBJS  := $(OBJ)/ax_low_2.o $(OBJ)/ax_low_3.o
-OBJS      := $(GEN_OBJS) $(FASTN_OBJS) $(LOW_OBJS) $(OBJ)/ax_fast.o $(OBJ)/ax_mma.o $(OBJ)/setup.o $(OBJ)/bp5.o $(OBJ)/capi.o
+PLANE_OBJS := $(OBJ)/ax_plane_3.o $(OBJ)/ax_plane_4.o
+OBJS      := $(GEN_OBJS) $(FASTN_OBJS) $(LOW_OBJS) $(PLANE_OBJS) $(OBJ)/ax_fast.o $(OBJ)/ax_mma.o $(OBJ)/setup.o $(OBJ)/bp5.o $(OBJ)/capi.o
 HEADERS   := $(SRC)/hx_common.cuh include/hx_axlocal.h $(wildcard $(SRC)/*.cuh)
 
 all: $(LIB)
@@ -24,6 +25,9 @@ $(OBJ)/ax_generic_%.o: $(SRC)/ax_generic.cu $(HEADERS) | $(OBJ)
 
 $(OBJ)/ax_low_%.o: $(SRC)/ax_low.cu $(HEADERS) | $(OBJ)
 	$(NVCC) $(NVFLAGS) -DHX_N1=$* -c $< -o $@
+
+$(OBJ)/ax_plane_%.o: $(SRC)/ax_plane.cu $(HEADERS) | $(OBJ)
+	$(NVCC) $(NVFLAGS) -fmad=false -DHX_N1=$* -c $< -o $@
 
 $(OBJ)/ax_fastn_%.o: $(SRC)/ax_fastn.cu $(HEADERS) | $(OBJ)
 	$(NVCC) $(NVFLAGS) -DHX_N1=$* -c $< -o $@

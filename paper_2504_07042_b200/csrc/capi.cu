@@ -53,6 +53,11 @@ HX_DECL_FASTN(16)
 cudaError_t hx_low_launch_2(const hx_axlocal_args*, cudaStream_t);
 cudaError_t hx_low_launch_3(const hx_axlocal_args*, cudaStream_t);
 cudaError_t hx_upload_basis_low_2(int, const double*, const double*, const double*);
+// j-plane kernels (ax_plane.cu) for orders 2, 3
+cudaError_t hx_plane_launch_3(const hx_axlocal_args*, cudaStream_t);
+cudaError_t hx_plane_launch_4(const hx_axlocal_args*, cudaStream_t);
+cudaError_t hx_upload_basis_plane_3(int, const double*, const double*, const double*);
+cudaError_t hx_upload_basis_plane_4(int, const double*, const double*, const double*);
 cudaError_t hx_upload_basis_low_3(int, const double*, const double*, const double*);
 cudaError_t hx_upload_basis_setup(int, const double*, const double*, const double*);
 cudaError_t hx_upload_basis_fast(int, const double*, const double*, const double*);
@@ -125,7 +130,7 @@ const upload_fn kUploads[] = {
     hx_upload_basis_generic_6,  hx_upload_basis_generic_7,  hx_upload_basis_generic_8,  hx_upload_basis_generic_9,
     hx_upload_basis_generic_10, hx_upload_basis_generic_11, hx_upload_basis_generic_12, hx_upload_basis_generic_13,
     hx_upload_basis_generic_14, hx_upload_basis_generic_15, hx_upload_basis_generic_16, hx_upload_basis_setup,
-    hx_upload_basis_fast,     hx_upload_basis_mma,
+    hx_upload_basis_fast,     hx_upload_basis_mma,     hx_upload_basis_plane_3,   hx_upload_basis_plane_4,
 };
 
 int fail(int code, const std::string& msg) {
@@ -243,6 +248,18 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n1 = a->order + 1;
+  // kernel 0 at orders 2 and 3: the j-plane kernel (ax_plane.cu) wherever it measures
+  // faster -- every source but parallelepiped at order 2 (element per thread) and
+  // stored at order 3 (order-generic); n_col 1 and 3 alike (profiles/r02_plane_ab.txt)
+  const bool plane_default = a->kernel == 0 && !a->gather &&
+                             ((n1 == 3 && a->factor_source != HX_PARALLELEPIPED) ||
+                              (n1 == 4 && a->factor_source != HX_STORED));
+  if (a->kernel == 5 || plane_default) {  // j-plane kernel (orders 2, 3)
+    if (a->gather) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the j-plane kernel");
+    if (n1 == 3) return cuda_status(hx_plane_launch_3(a, s), "hx_axlocal(plane)");
+    if (n1 == 4) return cuda_status(hx_plane_launch_4(a, s), "hx_axlocal(plane)");
+    return fail(HX_ERR_UNSUPPORTED, "kernel 5 (j-plane) covers orders 2 and 3");
+  }
   // kernel 0 at orders 1-2: the element-per-thread kernel wherever it measures fastest
   // (every source but stored; stored streams 6 factor fields per node and the
   // block-per-element kernels coalesce those better; profiles/r01_order_sweep.txt)

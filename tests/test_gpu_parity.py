@@ -21,13 +21,15 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 
 DEV = torch.device("cuda", 0)
 # 0 = best measured, 1 = slice kernel (Algorithm 4), 2 = fast kernel (specialised / order-generic),
-# 4 = DMMA kernel (order 7 only, ax_mma.cu)
-KERNELS = (0, 1, 2, 4)
+# 4 = DMMA kernel (order 7 only, ax_mma.cu), 5 = j-plane kernel (orders 2, 3, ax_plane.cu)
+KERNELS = (0, 1, 2, 4, 5)
 
 
 def _need(kernel, order):
     if kernel == 4 and order != 7:
         pytest.skip("kernel 4 (DMMA) covers order 7")
+    if kernel == 5 and order not in (2, 3):
+        pytest.skip("kernel 5 (j-plane) covers orders 2 and 3")
 
 
 def _op(c, elements, kernel):
@@ -186,6 +188,7 @@ def test_low_order_kernel_rejects_higher_orders():
 def test_ncol3_bitwise_equals_three_ncol1(kernel):
     """test_axlocal.py:206-225: factor reuse must not change per-column bits."""
     order = 7
+    _need(kernel, order)
     mesh = _random_box(order, 4, 3, 2, seed=9)
     rng = np.random.default_rng(1)
     x = torch.as_tensor(rng.standard_normal((mesh.n_elements, 512, 3)), device=DEV)
@@ -207,9 +210,40 @@ def test_ncol3_bitwise_equals_three_ncol1(kernel):
             assert torch.equal(y3[:, :, c], y1[:, :, 0]), (src, c)
 
 
+@pytest.mark.parametrize("kernel", [0, 5])
+@pytest.mark.parametrize("order", [2, 3])
+def test_ncol3_bitwise_small_orders(order, kernel):
+    """The j-plane kernel (and the default routing at orders 2, 3): n_col=3 == three
+    n_col=1 applies for every source and equation, and the oracle to 1e-12."""
+    mesh = _random_box(order, 5, 3, 2, seed=order)
+    E, n3 = mesh.n_elements, (order + 1) ** 3
+    rng = np.random.default_rng(order)
+    x = torch.as_tensor(rng.standard_normal((E, n3, 3)), device=DEV)
+    shear = np.array([[0.9, 0.2, -0.1], [0.0, 1.1, 0.3], [0.15, 0.0, 0.8]])
+    ppd = hx.box_mesh(5, 3, 2, order).vertices @ shear.T
+    kw = {"lam0": rng.uniform(0.5, 2.0, (E, n3)), "lam1": rng.uniform(0.5, 2.0, (E, n3))}
+    for eq, src in (("poisson", "trilinear"), ("poisson", "trilinear-partial"), ("poisson", "stored"),
+                    ("poisson", "parallelepiped"), ("helmholtz", "trilinear"), ("helmholtz", "trilinear-merged"),
+                    ("helmholtz", "stored"), ("helmholtz", "parallelepiped")):
+        verts = ppd if src == "parallelepiped" else mesh.vertices
+        k = kw if eq == "helmholtz" else {}
+        op3 = hx.LocalOperator(hx.KernelSpec(eq, 3, src, order), torch.as_tensor(verts, device=DEV),
+                               hx.SpectralBasis.build(order), **k)
+        op1 = hx.LocalOperator(hx.KernelSpec(eq, 1, src, order), torch.as_tensor(verts, device=DEV),
+                               hx.SpectralBasis.build(order), **k)
+        op3.kernel = op1.kernel = kernel
+        y3 = op3.apply(x)
+        want = O.apply(src, eq, order, verts, x.cpu().numpy(), k.get("lam0"), k.get("lam1"))
+        assert O.rel_diff(y3.cpu().numpy(), want) <= TOL, (eq, src)
+        for c in range(3):
+            y1 = op1.apply(x[:, :, c : c + 1].contiguous())
+            assert torch.equal(y3[:, :, c], y1[:, :, 0]), (eq, src, c)
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_run_to_run_bitwise(kernel):
     order = 7
+    _need(kernel, order)
     mesh = _random_box(order, 8, 8, 8, seed=4)
     op = hx.LocalOperator(hx.KernelSpec("poisson", 1, "trilinear", order), mesh, hx.SpectralBasis.build(order))
     op.kernel = kernel
@@ -390,6 +424,7 @@ def test_every_family_is_deterministic(order):
     mesh = _random_box(order, 5, 3, 2, pert=0.15, seed=order)
     n3 = (order + 1) ** 3
     kernels = (0, 1, 2, 3) if order <= 2 else (0, 1, 2, 4) if order == 7 else (0, 1, 2)
+    kernels += (5,) if order in (2, 3) else ()
     for eq, src, ncol in (("poisson", "trilinear", 1), ("helmholtz", "stored", 3), ("poisson", "trilinear-partial", 3)):
         kw = {"lam0": 1.1, "lam1": 0.7} if eq == "helmholtz" else {}
         x = torch.randn((mesh.n_elements, n3, ncol), dtype=torch.float64, device=DEV)

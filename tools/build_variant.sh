@@ -16,9 +16,9 @@ for o in build/obj/*.o; do
   hit=""
   for n in "$@"; do [ "$b" = "$n" ] && hit=1; done
   if [ -n "$hit" ]; then
-    src=${b%_*}; n1=${b##*_}; extra=""; [ "$b" = ax_mma ] && extra=-fmad=false
+    src=${b%_*}; n1=${b##*_}; extra=""; case $b in ax_mma|ax_plane_*) extra=-fmad=false;; esac
     case "$b" in
-      ax_fastn_*|ax_generic_*|ax_low_*) def="-DHX_N1=$n1"; srcf=paper_2504_07042_b200/csrc/$src.cu ;;
+      ax_fastn_*|ax_generic_*|ax_low_*|ax_plane_*) def="-DHX_N1=$n1"; srcf=paper_2504_07042_b200/csrc/$src.cu ;;
       *) def=""; srcf=paper_2504_07042_b200/csrc/$b.cu ;;
     esac
     nvcc -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -gencode arch=compute_100a,code=sm_100a \

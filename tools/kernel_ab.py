@@ -38,9 +38,10 @@ def main():
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--idle", type=float, default=0.3)
     ap.add_argument("--subset", type=int, default=256)
+    ap.add_argument("--order", type=int, default=7)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    order = 7
+    order = args.order
     ex, ey, ez = (int(v) for v in args.mesh.split(","))
     ppd = args.source == "parallelepiped"
     mesh = hx.box_mesh(ex, ey, ez, order, perturbation=0.0 if ppd else 0.1, seed=0)
@@ -100,6 +101,17 @@ def main():
             if h is not None:
                 clk[c].append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
     wc = workload_count(spec, include_dmat_traffic=False)
+    try:
+        import json
+
+        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9
+    except Exception:
+        hbm = 6.65e12
+
+    def roof_frac(ms):  # achieved / min(FP64, HBM) roofline, the reference's time model
+        t_bound = max((wc.f_ax + wc.f_geo) / 37.0e12, wc.m_bytes / hbm)
+        return E * t_bound / (ms * 1e-3)
+
     for c in cases:
         ts = sorted(times[c])
         ms = ts[len(ts) // 2]
@@ -107,7 +119,8 @@ def main():
         tf = E * (wc.f_ax + wc.f_geo) / (ms * 1e-3) / 1e12
         ck = sorted(clk[c]) or [0]
         print(f"kernel={c[0]} hook={c[1]:2d}: {ms:8.3f} ms {gd:7.1f} GDOF/s {tf:6.2f} TFLOP/s (frac of 37.0 TF "
-              f"{tf / 37.0:.3f}) spread {100 * (ts[-1] - ts[0]) / ms:4.1f}% clk {ck[len(ck) // 2]}", flush=True)
+              f"{tf / 37.0:.3f}; roofline frac {roof_frac(ms):.3f}) spread {100 * (ts[-1] - ts[0]) / ms:4.1f}% "
+              f"clk {ck[len(ck) // 2]}", flush=True)
 
 
 if __name__ == "__main__":

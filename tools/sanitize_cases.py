@@ -17,7 +17,8 @@ compute-sanitizer is closed on the GPU pool, so:
 ~64 elements per case.  Covers
 the N=7 kernels (DMMA ax8m n_col 1 / 3 (ax8m3) / fused lattice gather + CG
 update, ax8s, ax8c3), the order-generic role-table kernels (axn_r) at
-n1 = 4, 7, 11, the slice kernel, the element-per-thread kernel, the setup
+n1 = 4, 7, 11, the slice kernel, the element-per-thread kernel, the j-plane
+kernel (orders 2, 3), the setup
 kernels and the BP5 gather / scatter (scatter_band32_kernel) / mask / dot /
 CG-update kernels, every factor source and both equations.  The plain run
 also checks every case against the oracle (1e-12).
@@ -123,6 +124,12 @@ def main():
     for order in (1, 2):
         case(order, (4, 4, 4), "poisson", "trilinear", 3, 3)
         n += 1
+    # j-plane kernel (ax_plane.cu, kernel 5) at orders 2 and 3: every source, n_col 1 and 3
+    for order in (2, 3):
+        for eq, src in (("poisson", "trilinear"), ("poisson", "stored"), ("poisson", "parallelepiped"),
+                        ("helmholtz", "trilinear-merged"), ("helmholtz", "trilinear")):
+            case(order, (5, 3, 2), eq, src, 3 if src == "trilinear" else 1, 5)
+            n += 1
     # setup kernels (stored / partial / merged / ppd / validation / classification) ran above;
     # BP5: gather, scatter (band32 at N = 7), fused scatter + dot, mask, CG updates, fused-gather AxLocal
     for order, dims in ((7, (3, 2, 4)), (3, (4, 3, 2))):
