@@ -16,7 +16,9 @@
 //     live at a time.
 // 32 / n1 elements per warp (n1 = 3: lanes 30, 31 idle), no shared memory, no
 // barriers.  n_col = 3 runs each column in its own CTA row (blockIdx.y) with the
-// n_col = 1 arithmetic, so n_col = 3 == 3 x n_col = 1 bitwise.
+// n_col = 1 arithmetic, so n_col = 3 == 3 x n_col = 1 bitwise.  At n1 = 5 the 25
+// nodes per thread exhaust the register file (parallelepiped 138 vs 181 GDOF/s
+// for the order-generic kernel, measured); orders 4 and up stay there.
 #include "hx_common.cuh"
 
 #ifndef HX_N1
@@ -437,11 +439,14 @@ extern "C" cudaError_t HX_CAT(hx_plane_launch_, HX_N1)(const hx_axlocal_args* a,
   const bool helm = a->equation == HX_HELMHOLTZ;
   switch (a->factor_source) {
     case HX_TRILINEAR:
-      return helm ? launch<Tri<true, false, false>, true>(*a, s) : launch<Tri<false, false, false>, false>(*a, s);
     case HX_TRILINEAR_PARTIAL:
-      return launch<Tri<false, true, false>, false>(*a, s);
     case HX_TRILINEAR_MERGED:
-      return launch<Tri<true, false, true>, true>(*a, s);
+      if constexpr (N1 <= 4) {
+        if (a->factor_source == HX_TRILINEAR_PARTIAL) return launch<Tri<false, true, false>, false>(*a, s);
+        if (a->factor_source == HX_TRILINEAR_MERGED) return launch<Tri<true, false, true>, true>(*a, s);
+        return helm ? launch<Tri<true, false, false>, true>(*a, s) : launch<Tri<false, false, false>, false>(*a, s);
+      }
+      return cudaErrorNotSupported;
     case HX_STORED:
       return helm ? launch<Stored<true>, true>(*a, s) : launch<Stored<false>, false>(*a, s);
     case HX_PARALLELEPIPED:

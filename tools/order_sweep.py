@@ -2,15 +2,16 @@
 
     python tools/order_sweep.py [--dof 1e8] [--variants trilinear,parallelepiped,stored]
 
-With --cpu (default on) the reference algorithm (CPU oracle port, all host
-threads) is timed beside each (order, variant) on a sample of the same mesh's
-elements (sized for ~0.3 s of CPU work) and the GPU result is checked against
-it on that sample (rel_diff, the reference's metric).
+With --cpu (default on) the reference's CPU AxLocal -- the stock hosfem package
+from baseline/_ref when installed (tools/install_reference.sh), else the oracle
+port -- is timed with all host threads beside each (order, variant) on a sample
+of the same mesh's elements and the GPU result is checked against it on that
+sample (rel_diff, the reference's metric).
 
 Mesh per order: e^3 elements with e = round((dof / n1^3)^(1/3)), trilinear =
 box_mesh(e,e,e,N, pert 0.1, seed 0), parallelepiped = the unperturbed box under a global
 shear.  Prints GDOF/s and the fraction of the per-variant roofline (reference work model,
-D on chip; FP64 37.0 TF measured, HBM 6550 GB/s).
+D on chip; FP64 37.0 TF measured, HBM from MEASURED_PEAKS.json).
 """
 
 import argparse
@@ -25,7 +26,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2504_07042_b200 as hx  # noqa: E402
 from paper_2504_07042_b200.workload import workload_count  # noqa: E402
 
-FP64, HBM = 37.0e12, 6.5501e12
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FP64 = 37.0e12
+try:
+    HBM = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9
+except Exception:
+    HBM = 6.65e12
 
 
 def main():
@@ -61,7 +67,7 @@ def main():
                 if not args.no_cpu:
                     rows[-1].update(_cpu(var, order, verts, x, y))
                     r = rows[-1]
-                    print(f"        CPU[{r['cpu_threads']}t] {r['cpu_gdofs']:.4f} GDOF/s on {r['cpu_sample']} elements "
+                    print(f"        CPU[{r['cpu_kind']} {r['cpu_threads']}t] {r['cpu_gdofs']:.4f} GDOF/s on {r['cpu_sample']} elements "
                           f"-> GPU x{r['gdofs'] / r['cpu_gdofs']:.0f}; rel_diff {r['rel_diff']:.1e}", flush=True)
             del op, x, y, verts
             torch.cuda.empty_cache()
@@ -78,18 +84,42 @@ def _cpu(var, order, verts, x, y):
 
     n1 = order + 1
     threads = os.cpu_count() or 1
-    sample = int(max(threads, min(verts.shape[0], 4e6 // n1**3)))  # ~4 M DOF: ~0.1-0.5 s
+    sample = int(max(threads, min(verts.shape[0], 1e6 // n1**3)))  # ~1 M DOF: ~0.3-1 s for the stock package
     idx = torch.linspace(0, verts.shape[0] - 1, sample, device=verts.device).long()
     v = verts[idx].cpu().numpy()
     xs = x[idx].cpu().numpy()
-    st = O.setup(var, "poisson", order, v)
+    ref = _reference()
+    if ref is not None:
+        spec = ref.KernelSpec(ref.Equation.POISSON, 1, ref.FactorSource(var), order)
+        rop = ref.LocalOperator(spec, [ref.make_element(vv) for vv in v], ref.SpectralBasis.build(order))
+        field = ref.LocalField(xs, order)
+
+        def run():
+            return rop.apply(field, threads=threads).data
+        kind = "reference"
+    else:
+        st = O.setup(var, "poisson", order, v)
+
+        def run():
+            return O.apply_setup(st, xs, threads=threads)
+        kind = "port"
     best = float("inf")
     for _ in range(2):
         t0 = time.perf_counter()
-        want = O.apply_setup(st, xs, threads=threads)
+        want = run()
         best = min(best, time.perf_counter() - t0)
-    return dict(cpu_gdofs=sample * n1**3 / best / 1e9, cpu_threads=threads, cpu_sample=sample,
+    return dict(cpu_gdofs=sample * n1**3 / best / 1e9, cpu_threads=threads, cpu_sample=sample, cpu_kind=kind,
                 rel_diff=O.rel_diff(y[idx].cpu().numpy(), want))
+
+
+def _reference():
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "hosfem")):
+        return None
+    sys.path.insert(0, ref_dir)
+    import hosfem
+
+    return hosfem
 
 
 def _time(op, x, y, spec, E, order, var, kern, reps):
@@ -109,7 +139,8 @@ def _time(op, x, y, spec, E, order, var, kern, reps):
     t_model = max((wc.f_ax + wc.f_geo) / FP64, wc.m_bytes / HBM) * E
     frac = t_model / (ms * 1e-3)
     gdofs = E * n1**3 / (ms * 1e-3) / 1e9
-    kernel = {0: "best", 1: "slice", 2: "specialised" if order == 7 else "fast", 3: "thread-per-element"}[kern]
+    kernel = {0: "best", 1: "slice", 2: "specialised" if order == 7 else "fast", 3: "thread-per-element",
+              4: "dmma", 5: "j-plane"}[kern]
     print(f"N={order:2d} {var:15s} E={E:9d} ({E * n1**3 / 1e6:6.1f} M DOF) {ms:8.3f} ms "
           f"{gdofs:7.1f} GDOF/s  {100 * frac:5.1f}% of roofline  [{kernel}]", flush=True)
     return dict(order=order, variant=var, elements=E, dof=E * n1**3, ms=ms, gdofs=gdofs, roofline_frac=frac,
