@@ -281,16 +281,24 @@ struct Tri {
       }
     }
   }
+  struct Fld {
+    double2 l0, l1;
+  };
+  template <int K>
+  __device__ __forceinline__ void load(const Lane& L, Fld& fl) const {
+    if (HELM) {
+      const int n = K * 64 + L.g * 8 + 2 * L.q;
+      fl.l0 = lam0 ? ld2(lam0 + n) : make_double2(l0v, l0v);
+      fl.l1 = lam1 ? ld2(lam1 + n) : make_double2(l1v, l1v);
+    }
+  }
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo& S, const Lane& L, const double x0[2], const double x1[2],
                                         const double x2[2], const double xk[2], double rr[2], double ss[2],
-                                        double tt[2], double ms[2]) const {
+                                        double tt[2], double ms[2], const Fld& fl) const {
     const double a00 = S.t00[K][L.g];
     const double2 a11 = *reinterpret_cast<const double2*>(&S.t11[K][2 * L.q]);
-    double2 l0 = make_double2(l0v, l0v), l1 = make_double2(l1v, l1v);
-    const int n = K * 64 + L.g * 8 + 2 * L.q;
-    if (HELM && lam0) l0 = ld2(lam0 + n);
-    if (HELM && lam1) l1 = ld2(lam1 + n);
+    const double2 l0 = fl.l0, l1 = fl.l1;
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       double g[6], dt;
@@ -351,16 +359,22 @@ struct TriStoredScale {
     sa = (MERGED ? a.lam2 : a.lam_geo) + L.e * N3;
     sb = MERGED ? a.lam3 + L.e * N3 : nullptr;
   }
+  struct Fld {
+    double2 s2, m2;
+  };
+  template <int K>
+  __device__ __forceinline__ void load(const Lane& L, Fld& fl) const {
+    const int n = K * 64 + L.g * 8 + 2 * L.q;
+    fl.s2 = ld2(sa + n);
+    fl.m2 = MERGED ? ld2(sb + n) : make_double2(0.0, 0.0);
+  }
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo& S, const Lane& L, const double x0[2], const double x1[2],
                                         const double x2[2], const double xk[2], double rr[2], double ss[2],
-                                        double tt[2], double ms[2]) const {
+                                        double tt[2], double ms[2], const Fld& fl) const {
     const double a00 = S.t00[K][L.g];
     const double2 a11 = *reinterpret_cast<const double2*>(&S.t11[K][2 * L.q]);
-    const int n = K * 64 + L.g * 8 + 2 * L.q;
-    const double2 s2 = ld2(sa + n);
-    double2 m2 = make_double2(0.0, 0.0);
-    if (MERGED) m2 = ld2(sb + n);
+    const double2 s2 = fl.s2, m2 = fl.m2;
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       double g[6];
@@ -396,10 +410,13 @@ template <typename F>
 struct FacLoaded {
   static constexpr bool kTri = true, kWFold = F::kWFold;
   const double2 (*fac)[F::kNF][32];
+  struct Fld {};  // loads stay in the slice
+  template <int K>
+  __device__ __forceinline__ void load(const Lane&, Fld&) const {}
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo&, const Lane& L, const double x0[2], const double x1[2],
                                         const double x2[2], const double xk[2], double rr[2], double ss[2],
-                                        double tt[2], double ms[2]) const {
+                                        double tt[2], double ms[2], const Fld& fl) const {
     const int lane = L.g * 4 + L.q;
     double v0[F::kNF], v1[F::kNF];
 #pragma unroll
@@ -433,14 +450,22 @@ struct Ppd {
       l1v = a.lam1_value;
     }
   }
+  struct Fld {
+    double2 l0, l1;
+  };
+  template <int K>
+  __device__ __forceinline__ void load(const Lane& L, Fld& fl) const {
+    if (HELM) {
+      const int n = K * 64 + L.g * 8 + 2 * L.q;
+      fl.l0 = lam0 ? ld2(lam0 + n) : make_double2(l0v, l0v);
+      fl.l1 = lam1 ? ld2(lam1 + n) : make_double2(l1v, l1v);
+    }
+  }
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo&, const Lane& L, const double x0[2], const double x1[2],
                                         const double x2[2], const double xk[2], double rr[2], double ss[2],
-                                        double tt[2], double ms[2]) const {
-    double2 l0 = make_double2(l0v, l0v), l1 = make_double2(l1v, l1v);
-    const int n = K * 64 + L.g * 8 + 2 * L.q;
-    if (HELM && lam0) l0 = ld2(lam0 + n);
-    if (HELM && lam1) l1 = ld2(lam1 + n);
+                                        double tt[2], double ms[2], const Fld& fl) const {
+    const double2 l0 = fl.l0, l1 = fl.l1;
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       symv(h[0], h[1], h[2], h[3], h[4], h[5], wji[b], x0[b], x1[b], x2[b], rr[b], ss[b], tt[b]);
@@ -474,10 +499,13 @@ struct Stored {
       l1v = a.lam1_value;
     }
   }
+  struct Fld {};  // loads stay in the slice
+  template <int K>
+  __device__ __forceinline__ void load(const Lane&, Fld&) const {}
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo&, const Lane& L, const double x0[2], const double x1[2],
                                         const double x2[2], const double xk[2], double rr[2], double ss[2],
-                                        double tt[2], double ms[2]) const {
+                                        double tt[2], double ms[2], const Fld& fl) const {
     const int n = K * 64 + L.g * 8 + 2 * L.q;
     double2 gg[6];
 #pragma unroll
@@ -607,6 +635,8 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
   // forward r / s derivatives of slice K (two chained DMMAs each)
 #define HX_FWD(K, X0, X1)                                               \
   double X0[2], X1[2];                                                  \
+  typename F::Fld X0##_fl;                                              \
+  fac.template load<K>(L, X0##_fl); /* fields one pipeline step ahead */ \
   {                                                                     \
     dmma(X0[0], X0[1], xa[K], Dr[0], 0.0, 0.0);                         \
     dmma(X0[0], X0[1], xb[K], Dr[1], X0[0], X0[1]);                     \
@@ -619,7 +649,7 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
   {                                                                                      \
     double x2[2] = {ta[K], tb[K]}, xk[2] = {xa[K], xb[K]};                               \
     double rr[2], ss[2], tt[2], ms[2] = {0.0, 0.0};                                      \
-    fac.template slice<K>(S, L, X0, X1, x2, xk, rr, ss, tt, ms);                         \
+    fac.template slice<K>(S, L, X0, X1, x2, xk, rr, ss, tt, ms, X0##_fl);               \
     ta[K] = tt[0];                                                                       \
     tb[K] = tt[1];                                                                       \
     double* tl = tiles[K & 1];                                                           \
@@ -907,7 +937,11 @@ extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
     return cudaErrorNotSupported;  // the lattice gather is built for the trilinear Poisson sources
   switch (a->factor_source) {
     case HX_TRILINEAR:
-      if (helm) return launch<Tri<true>>(*a, s);
+      if (helm) {
+        // 232 registers: 114 GDOF/s vs 100 at 168 (still below ax8s, profiles/r02_mma_fields_ab.txt)
+        if (a->reserved == 65) return launch<Tri<true>, 232>(*a, s);
+        return launch<Tri<true>>(*a, s);
+      }
       switch (a->reserved) {  // register-cap A/B (tools/kernel_ab.py)
         case 61: return launch<Tri<false>, 160>(*a, s);
         case 62: return launch<Tri<false>, 152>(*a, s);

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--idle", type=float, default=0.3)
     ap.add_argument("--subset", type=int, default=256)
     ap.add_argument("--order", type=int, default=7)
+    ap.add_argument("--fields", action="store_true", help="Helmholtz lam0 / lam1 as (E, n1^3) fields")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     order = args.order
@@ -53,6 +54,10 @@ def main():
     n3 = (order + 1) ** 3
     nc = args.n_col
     kw = {"lam0": 1.3, "lam1": 0.4} if args.equation == "helmholtz" else {}
+    if kw and args.fields:
+        gf = torch.Generator(device=dev).manual_seed(5)
+        kw = {k: torch.rand((E, (order + 1) ** 3), dtype=torch.float64, device=dev, generator=gf) + 0.5
+              for k in ("lam0", "lam1")}
     spec = hx.KernelSpec(args.equation, nc, args.source, order)
     op = hx.LocalOperator(spec, verts, hx.SpectralBasis.build(order), device=dev, **kw)
     g = torch.Generator(device=dev).manual_seed(0)
@@ -63,7 +68,9 @@ def main():
     sub = np.sort(rng.choice(E, size=min(args.subset, E), replace=False))
     vh = verts[torch.as_tensor(sub, device=dev)].cpu().numpy()
     xh = x[torch.as_tensor(sub, device=dev)].cpu().numpy()
-    want = O.apply(args.source, args.equation, order, vh, xh, **kw)
+    idx = torch.as_tensor(sub, device=dev)
+    kwh = {k: (v[idx].cpu().numpy() if torch.is_tensor(v) else v) for k, v in kw.items()}
+    want = O.apply(args.source, args.equation, order, vh, xh, **kwh)
     for kernel, hook in cases:
         a = op._args(x.data_ptr(), y.data_ptr())
         a.kernel, a.reserved = kernel, hook
@@ -108,7 +115,7 @@ def main():
     except Exception:
         hbm = 6.65e12
 
-    def roof_frac(ms):  # achieved / min(FP64, HBM) roofline, the reference's time model
+    def roof_frac(ms):  # achieved / min(FP64, HBM) roofline; Helmholtz charged with fields (--fields)
         t_bound = max((wc.f_ax + wc.f_geo) / 37.0e12, wc.m_bytes / hbm)
         return E * t_bound / (ms * 1e-3)
 

@@ -9,7 +9,11 @@ scalar-coefficient run never makes (the r01 table's fractions above 1).
 Bounds: 37.0 TFLOP/s FP64 (measured DFMA = DMMA peak, profiles/r01_ubench_fp64.txt)
 and the driver-measured copy bandwidth (MEASURED_PEAKS.json), D on chip.
 Timing: per case, rounds of 20 back-to-back launches after 3 warm-ups and a
-0.3 s idle (median of 3 rounds), CUDA events, inputs larger than L2.
+0.3 s idle (median of 3 rounds), CUDA events, inputs larger than L2.  The SM
+clock and throttle reasons are sampled (NVML) while the launches run: the
+field-reading Helmholtz rows run at the power cap (sw_power_cap, SM clock well
+below 1965 MHz), so their FP64 fraction at the clock they ran at is higher
+than the nominal-clock fraction printed.
 """
 
 import argparse
@@ -19,6 +23,27 @@ import sys
 import time
 
 import torch
+
+try:
+    import pynvml
+
+    pynvml.nvmlInit()
+    _NVML = pynvml.nvmlDeviceGetHandleByIndex(0)
+except Exception:
+    _NVML = None
+
+
+def _clock_sample():
+    """(SM MHz, throttle-reason bits) now, or (0, 0) without NVML."""
+    if _NVML is None:
+        return 0, 0
+    return (pynvml.nvmlDeviceGetClockInfo(_NVML, pynvml.NVML_CLOCK_SM),
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(_NVML))
+
+
+def _reason_names(bits):
+    names = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal", 0x40: "hw_thermal", 0x80: "hw_power_brake"}
+    return ",".join(v for k, v in names.items() if bits & k) or "-"
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -61,7 +86,7 @@ def main():
     print(f"# N=7 variants at box {ex}x{ey}x{ez} = {E} elements; Helmholtz with lam0 / lam1 fields; "
           f"roofline at {fp64 / 1e12:.1f} TFLOP/s and {hbm / 1e9:.1f} GB/s")
     print(f"{'equation':9s} {'n_col':>5s} {'source':18s} {'kernel':>6s} {'ms':>8s} {'GDOF/s':>8s} "
-          f"{'roof GDOF/s':>11s} {'frac':>6s}  bound")
+          f"{'roof GDOF/s':>11s} {'frac':>6s}  bound {'SM MHz':>6s}  reasons")
     for eq, nc, src in CASES:
         verts = ppd if src == "parallelepiped" else tri
         kw = {"lam0": lam0, "lam1": lam1} if eq == "helmholtz" else {}
@@ -75,7 +100,7 @@ def main():
         roof = E * n3 * nc / (E * max(t_cmp, t_mem)) / 1e9
         for kernel in (int(k) for k in args.kernels.split(",")):
             op.kernel = kernel
-            ts = []
+            ts, clks, bits = [], [], 0
             for _ in range(args.rounds):
                 for _ in range(3):
                     op.apply_(xv, yv)
@@ -86,12 +111,18 @@ def main():
                 for _ in range(args.reps):
                     op.apply_(xv, yv)
                 e.record()
+                for _ in range(4):  # the launches are queued: sample while they run
+                    time.sleep(0.01)
+                    c, b = _clock_sample()
+                    clks.append(c)
+                    bits |= b
                 e.synchronize()
                 ts.append(s.elapsed_time(e) / args.reps)
             ms = sorted(ts)[len(ts) // 2]
             g = E * n3 * nc / (ms * 1e-3) / 1e9
             print(f"{eq:9s} {nc:5d} {src:18s} {kernel:6d} {ms:8.3f} {g:8.1f} {roof:11.1f} {g / roof:6.3f}  "
-                  f"{'FP64' if t_cmp >= t_mem else 'HBM'}", flush=True)
+                  f"{'FP64' if t_cmp >= t_mem else 'HBM':5s} {sorted(clks)[len(clks) // 2]:6d}  {_reason_names(bits)}",
+                  flush=True)
         del op, xv, yv
         torch.cuda.empty_cache()
 
