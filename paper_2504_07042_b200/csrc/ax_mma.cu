@@ -132,6 +132,9 @@ struct Lane {
 };
 
 __device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+// L1 prefetch (no register): ptxas sinks the field loads to ~50 instructions
+// before their use at this register cap, so the line is fetched a slice earlier.
+__device__ __forceinline__ void pf_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // (rr, ss, tt) = G (s x0, s x1, s x2) with G symmetric, the reference's row order.
 __device__ __forceinline__ void symv(double g0, double g1, double g2, double g3, double g4, double g5, double s,
@@ -290,6 +293,8 @@ struct Tri {
       const int n = K * 64 + L.g * 8 + 2 * L.q;
       fl.l0 = lam0 ? ld2(lam0 + n) : make_double2(l0v, l0v);
       fl.l1 = lam1 ? ld2(lam1 + n) : make_double2(l1v, l1v);
+      if (K + 1 < N1 && lam0) pf_l1(lam0 + n + 64);
+      if (K + 1 < N1 && lam1) pf_l1(lam1 + n + 64);
     }
   }
   template <int K>
@@ -367,6 +372,10 @@ struct TriStoredScale {
     const int n = K * 64 + L.g * 8 + 2 * L.q;
     fl.s2 = ld2(sa + n);
     fl.m2 = MERGED ? ld2(sb + n) : make_double2(0.0, 0.0);
+    if (K + 1 < N1 && MERGED) {  // partial: -1.3 % with it, merged +1.5 % (profiles/r02_mma_fields_ab.txt)
+      pf_l1(sa + n + 64);
+      pf_l1(sb + n + 64);
+    }
   }
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo& S, const Lane& L, const double x0[2], const double x1[2],
@@ -459,6 +468,8 @@ struct Ppd {
       const int n = K * 64 + L.g * 8 + 2 * L.q;
       fl.l0 = lam0 ? ld2(lam0 + n) : make_double2(l0v, l0v);
       fl.l1 = lam1 ? ld2(lam1 + n) : make_double2(l1v, l1v);
+      if (K + 1 < N1 && lam0) pf_l1(lam0 + n + 64);
+      if (K + 1 < N1 && lam1) pf_l1(lam1 + n + 64);
     }
   }
   template <int K>
@@ -719,16 +730,19 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
   }
 }
 
-// NREG: register cap (__maxnreg__); 65536 / (32 NREG) warps per SM are resident
-template <typename F, int NCOL, int NREG, bool GATHER = false, bool CGP = false>
+// NREG: register cap (__maxnreg__); 65536 / (32 NREG) warps per SM are resident.
+// n_col = 3: one warp per (element, column), each the n_col = 1 arithmetic;
+// CTA3: the element's three column warps in one CTA (one SM, so the strided
+// column loads of x share L1 lines), else one CTA per (element, column).
+template <typename F, int NCOL, int NREG, bool GATHER = false, bool CGP = false, bool CTA3 = false>
 __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a) {
   constexpr int MINB = 65536 / (32 * NREG);
-  __shared__ ElemGeo S;
-  const int lane = threadIdx.x;
-  // n_col = 3: one warp per (element, column), each the n_col = 1 arithmetic
-  const int col = NCOL == 1 ? 0 : (int)(blockIdx.x % NCOL);
+  __shared__ ElemGeo S_[CTA3 ? NCOL : 1];
+  const int lane = threadIdx.x & 31;
+  const int col = NCOL == 1 ? 0 : CTA3 ? (int)(threadIdx.x >> 5) : (int)(blockIdx.x % NCOL);
+  ElemGeo& S = S_[CTA3 ? col : 0];
   Lane L;
-  L.e = NCOL == 1 ? (int64_t)blockIdx.x : (int64_t)(blockIdx.x / NCOL);
+  L.e = NCOL == 1 || CTA3 ? (int64_t)blockIdx.x : (int64_t)(blockIdx.x / NCOL);
   L.g = lane >> 2;
   L.q = lane & 3;
 
@@ -914,7 +928,10 @@ cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
         return cudaGetLastError();
       }
     }
-    ax8m<F, 3, NREG><<<grid, 32, 0, s>>>(a);
+    if (a.reserved == 72)  // 72: one CTA per (element, column) (A/B)
+      ax8m<F, 3, NREG><<<grid, 32, 0, s>>>(a);
+    else
+      ax8m<F, 3, NREG, false, false, true><<<(unsigned)a.n_elements, 96, 0, s>>>(a);
   }
   else
     ax8m<F, 1, NREG><<<grid, 32, 0, s>>>(a);

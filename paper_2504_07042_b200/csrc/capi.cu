@@ -269,17 +269,18 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
     if (a->gather) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the low-order kernel");
     return cuda_status(n1 == 2 ? hx_low_launch_2(a, s) : hx_low_launch_3(a, s), "hx_axlocal(low)");
   }
-  // kernel 0 at order 7: the DMMA kernel (ax_mma.cu) for the Poisson sources
-  // where it measures fastest -- trilinear and trilinear-partial (also with the
-  // fused BP5 lattice gather, so fused and unfused stay bitwise equal) and
-  // parallelepiped -- at n_col 1 and 3 alike, so that n_col = 3 stays bitwise
-  // three n_col = 1 applies; ax8s / ax8c3 for stored and every Helmholtz source
-  // (profiles/r02_n7_variants_c4.txt)
+  // kernel 0 at order 7: the DMMA kernel (ax_mma.cu) where it measures fastest
+  // -- Poisson trilinear and trilinear-partial (also with the fused BP5
+  // lattice gather, so fused and unfused stay bitwise equal) and
+  // parallelepiped of both equations -- at n_col 1 and 3 alike, so that
+  // n_col = 3 stays bitwise three n_col = 1 applies; ax8s / ax8c3 for stored
+  // and the Helmholtz trilinear sources (profiles/r02_n7_variants_c4.txt)
   const bool helm_eq = a->equation == HX_HELMHOLTZ;
   const bool mma_default =
-      a->kernel == 0 && a->order == 7 && !helm_eq &&
-      (a->factor_source == HX_TRILINEAR || a->factor_source == HX_TRILINEAR_PARTIAL ||
-       (a->factor_source == HX_PARALLELEPIPED && !a->gather));
+      a->kernel == 0 && a->order == 7 &&
+      (helm_eq ? a->factor_source == HX_PARALLELEPIPED
+               : (a->factor_source == HX_TRILINEAR || a->factor_source == HX_TRILINEAR_PARTIAL ||
+                  (a->factor_source == HX_PARALLELEPIPED && !a->gather)));
   if (a->kernel == 4 || mma_default) {  // DMMA kernel (order 7, element-local x)
     cudaError_t e = hx_mma_launch(a, s);
     if (e != cudaErrorNotSupported) return cuda_status(e, "hx_axlocal(mma)");

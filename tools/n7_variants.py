@@ -8,7 +8,7 @@ base_memory_reals) counts two per-node coefficient reads for Helmholtz, which a
 scalar-coefficient run never makes (the r01 table's fractions above 1).
 Bounds: 37.0 TFLOP/s FP64 (measured DFMA = DMMA peak, profiles/r01_ubench_fp64.txt)
 and the driver-measured copy bandwidth (MEASURED_PEAKS.json), D on chip.
-Timing: per case, rounds of 20 back-to-back launches after 3 warm-ups and a
+Timing: per case, rounds of 40 back-to-back launches after 3 warm-ups and a
 0.3 s idle (median of 3 rounds), CUDA events, inputs larger than L2.  The SM
 clock and throttle reasons are sampled (NVML) while the launches run: the
 field-reading Helmholtz rows run at the power cap (sw_power_cap, SM clock well
@@ -62,7 +62,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mesh", default="128,128,96")
     ap.add_argument("--kernels", default="0")
-    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--reps", type=int, default=40)
     ap.add_argument("--rounds", type=int, default=3)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -111,8 +111,8 @@ def main():
                 for _ in range(args.reps):
                     op.apply_(xv, yv)
                 e.record()
-                for _ in range(4):  # the launches are queued: sample while they run
-                    time.sleep(0.01)
+                while not e.query():  # the launches are queued: sample until they finish
+                    time.sleep(0.02)
                     c, b = _clock_sample()
                     clks.append(c)
                     bits |= b
