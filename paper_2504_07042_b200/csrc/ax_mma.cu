@@ -132,9 +132,6 @@ struct Lane {
 };
 
 __device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
-// L1 prefetch (no register): ptxas sinks the field loads to ~50 instructions
-// before their use at this register cap, so the line is fetched a slice earlier.
-__device__ __forceinline__ void pf_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // (rr, ss, tt) = G (s x0, s x1, s x2) with G symmetric, the reference's row order.
 __device__ __forceinline__ void symv(double g0, double g1, double g2, double g3, double g4, double g5, double s,
@@ -284,6 +281,12 @@ struct Tri {
       }
     }
   }
+  // lam0 / lam1 fields staged in shared memory by the kernel (bulk copy per element)
+  static constexpr int kStage = HELM ? 2 : 0;
+  __device__ __forceinline__ static const double* stage_base(const hx_axlocal_args& a, int f) {
+    return f == 0 ? a.lam0 : a.lam1;
+  }
+  const double* sf;
   struct Fld {
     double2 l0, l1;
   };
@@ -291,10 +294,8 @@ struct Tri {
   __device__ __forceinline__ void load(const Lane& L, Fld& fl) const {
     if (HELM) {
       const int n = K * 64 + L.g * 8 + 2 * L.q;
-      fl.l0 = lam0 ? ld2(lam0 + n) : make_double2(l0v, l0v);
-      fl.l1 = lam1 ? ld2(lam1 + n) : make_double2(l1v, l1v);
-      if (K + 1 < N1 && lam0) pf_l1(lam0 + n + 64);
-      if (K + 1 < N1 && lam1) pf_l1(lam1 + n + 64);
+      fl.l0 = lam0 ? *reinterpret_cast<const double2*>(sf + n) : make_double2(l0v, l0v);
+      fl.l1 = lam1 ? *reinterpret_cast<const double2*>(sf + N3 + n) : make_double2(l1v, l1v);
     }
   }
   template <int K>
@@ -338,7 +339,7 @@ struct Tri {
     double sc = tri_rdet<K>(f[b], dt);
     if (HELM) {
       const int n = K * 64 + L.g * 8 + 2 * L.q + b;
-      const double l0 = lam0 ? __ldg(lam0 + n) : l0v, l1 = lam1 ? __ldg(lam1 + n) : l1v;
+      const double l0 = lam0 ? sf[n] : l0v, l1 = lam1 ? sf[N3 + n] : l1v;
       v[7] = l1 * (dt * cm[b]);
       sc = l0 * sc;
     }
@@ -364,18 +365,20 @@ struct TriStoredScale {
     sa = (MERGED ? a.lam2 : a.lam_geo) + L.e * N3;
     sb = MERGED ? a.lam3 + L.e * N3 : nullptr;
   }
+  // the stored scale(s) staged in shared memory by the kernel (bulk copy per element)
+  static constexpr int kStage = MERGED ? 2 : 1;
+  __device__ __forceinline__ static const double* stage_base(const hx_axlocal_args& a, int f) {
+    return MERGED ? (f == 0 ? a.lam2 : a.lam3) : a.lam_geo;
+  }
+  const double* sf;
   struct Fld {
     double2 s2, m2;
   };
   template <int K>
   __device__ __forceinline__ void load(const Lane& L, Fld& fl) const {
     const int n = K * 64 + L.g * 8 + 2 * L.q;
-    fl.s2 = ld2(sa + n);
-    fl.m2 = MERGED ? ld2(sb + n) : make_double2(0.0, 0.0);
-    if (K + 1 < N1 && MERGED) {  // partial: -1.3 % with it, merged +1.5 % (profiles/r02_mma_fields_ab.txt)
-      pf_l1(sa + n + 64);
-      pf_l1(sb + n + 64);
-    }
+    fl.s2 = *reinterpret_cast<const double2*>(sf + n);
+    fl.m2 = MERGED ? *reinterpret_cast<const double2*>(sf + N3 + n) : make_double2(0.0, 0.0);
   }
   template <int K>
   __device__ __forceinline__ void slice(const ElemGeo& S, const Lane& L, const double x0[2], const double x1[2],
@@ -403,8 +406,8 @@ struct TriStoredScale {
   __device__ __forceinline__ void node_factors(const ElemGeo& S, const Lane& L, int b, double v[kNF]) const {
     tri_adj<K>(f[b], S.t00[K][L.g], S.t11[K][2 * L.q + b], v);
     const int n = K * 64 + L.g * 8 + 2 * L.q + b;
-    v[6] = __ldg(sa + n);
-    if (MERGED) v[7] = __ldg(sb + n);
+    v[6] = sf[n];
+    if (MERGED) v[7] = sf[N3 + n];
   }
   __device__ __forceinline__ static void apply(const double v[kNF], double x0, double x1, double x2, double xk,
                                                double& rr, double& ss, double& tt, double& ms) {
@@ -419,6 +422,9 @@ template <typename F>
 struct FacLoaded {
   static constexpr bool kTri = true, kWFold = F::kWFold;
   const double2 (*fac)[F::kNF][32];
+  static constexpr int kStage = 0;
+  __device__ __forceinline__ static const double* stage_base(const hx_axlocal_args&, int) { return nullptr; }
+  const double* sf;
   struct Fld {};  // loads stay in the slice
   template <int K>
   __device__ __forceinline__ void load(const Lane&, Fld&) const {}
@@ -459,6 +465,12 @@ struct Ppd {
       l1v = a.lam1_value;
     }
   }
+  // lam0 / lam1 fields staged in shared memory by the kernel (bulk copy per element)
+  static constexpr int kStage = HELM ? 2 : 0;
+  __device__ __forceinline__ static const double* stage_base(const hx_axlocal_args& a, int f) {
+    return f == 0 ? a.lam0 : a.lam1;
+  }
+  const double* sf;
   struct Fld {
     double2 l0, l1;
   };
@@ -466,10 +478,8 @@ struct Ppd {
   __device__ __forceinline__ void load(const Lane& L, Fld& fl) const {
     if (HELM) {
       const int n = K * 64 + L.g * 8 + 2 * L.q;
-      fl.l0 = lam0 ? ld2(lam0 + n) : make_double2(l0v, l0v);
-      fl.l1 = lam1 ? ld2(lam1 + n) : make_double2(l1v, l1v);
-      if (K + 1 < N1 && lam0) pf_l1(lam0 + n + 64);
-      if (K + 1 < N1 && lam1) pf_l1(lam1 + n + 64);
+      fl.l0 = lam0 ? *reinterpret_cast<const double2*>(sf + n) : make_double2(l0v, l0v);
+      fl.l1 = lam1 ? *reinterpret_cast<const double2*>(sf + N3 + n) : make_double2(l1v, l1v);
     }
   }
   template <int K>
@@ -510,6 +520,9 @@ struct Stored {
       l1v = a.lam1_value;
     }
   }
+  static constexpr int kStage = 0;
+  __device__ __forceinline__ static const double* stage_base(const hx_axlocal_args&, int) { return nullptr; }
+  const double* sf;
   struct Fld {};  // loads stay in the slice
   template <int K>
   __device__ __forceinline__ void load(const Lane&, Fld&) const {}
@@ -746,6 +759,31 @@ __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a
   L.g = lane >> 2;
   L.q = lane & 3;
 
+  // the element's per-node field arrays (F::kStage of them: Helmholtz lam0 /
+  // lam1, the stored scales of partial / merged) land in shared memory by one
+  // bulk copy each, issued first and waited for after the geometry prologue:
+  // no registers held for them and no load latency inside the slices
+  // (one copy per CTA: the CTA3 column warps share it)
+  constexpr int NS = F::kStage;
+  __shared__ alignas(128) double sf[NS > 0 ? NS * N3 : 2];
+  __shared__ uint64_t bar[1];
+  bool staged = false;
+  if constexpr (NS > 0) {
+#pragma unroll
+    for (int f = 0; f < NS; ++f) staged |= F::stage_base(a, f) != nullptr;
+    if (staged && threadIdx.x == 0) {
+      uint32_t bytes = 0;
+#pragma unroll
+      for (int f = 0; f < NS; ++f) bytes += F::stage_base(a, f) ? 8u * N3 : 0u;
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar, bytes);
+#pragma unroll
+      for (int f = 0; f < NS; ++f)
+        if (const double* src = F::stage_base(a, f)) bulk_g2s(sf + f * N3, src + L.e * N3, 8u * N3, bar);
+    }
+  }
+
   // warm L2 with the element ~1.25 waves of resident warps ahead: x, vertices,
   // and the per-node fields of the variants that stream them
   if (lane < 2 && col == 0) {
@@ -799,7 +837,10 @@ __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a
   }
   F fac;
   fac.prepare(a, S, L);
-  if (F::kTri) __syncwarp();
+  fac.sf = sf;
+  if (F::kTri || NS > 0) __syncwarp();
+  if constexpr (CTA3 && NS > 0) __syncthreads();  // the barrier's init, for the other warps
+  if (NS > 0 && staged) mbar_wait(bar, 0);
   column<F, NCOL, GATHER, CGP>(a, S, S.tile, fac, L, X, xa, xb, Dr, Ds, Dt, Dy, col);
 }
 
@@ -821,6 +862,26 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
   L.e = blockIdx.x;
   L.g = lane >> 2;
   L.q = lane & 3;
+  // the per-node fields of the factor phase, staged as in ax8m
+  constexpr int NS = F::kStage;
+  __shared__ alignas(128) double sf[NS > 0 ? NS * N3 : 2];
+  __shared__ uint64_t bar[1];
+  bool staged = false;
+  if constexpr (NS > 0) {
+#pragma unroll
+    for (int f = 0; f < NS; ++f) staged |= F::stage_base(a, f) != nullptr;
+    if (staged && threadIdx.x == 0) {
+      uint32_t bytes = 0;
+#pragma unroll
+      for (int f = 0; f < NS; ++f) bytes += F::stage_base(a, f) ? 8u * N3 : 0u;
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar, bytes);
+#pragma unroll
+      for (int f = 0; f < NS; ++f)
+        if (const double* src = F::stage_base(a, f)) bulk_g2s(sf + f * N3, src + L.e * N3, 8u * N3, bar);
+    }
+  }
   if (threadIdx.x < 2) {
     const int64_t ahead = L.e + (int64_t)148 * MINB * HX_MMA_AHEAD_WAVES4 / 4 / 3;
     if (ahead < a.n_elements) {
@@ -852,6 +913,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
   __syncthreads();
   {
     F fac;
+    fac.sf = sf;
 #ifdef HX_MMA3_FIBRE_SPLIT  // warps 0 / 1 one fibre each, all slices (A/B: -3 %)
     if (w < 2) {
       fac.prepare_one(a, S, L, w);
@@ -860,6 +922,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
       tri_tables(S, lane & 7, 4 + (lane >> 3));
     }
     __syncthreads();
+    if (NS > 0 && staged && w < 2) mbar_wait(bar, 0);
     if (w < 2) {
       double* dst = reinterpret_cast<double*>(&s_fac[0][0][lane]) + w;
 #define HX_FAC(K)                                                        \
@@ -881,6 +944,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
       tri_tables(S, lane & 7, 4 + (lane >> 3));
     }
     __syncthreads();
+    if (NS > 0 && staged && w < 2) mbar_wait(bar, 0);
 #define HX_FAC(K)                                                        \
   {                                                                      \
     double v0[F::kNF], v1[F::kNF];                                       \
@@ -942,13 +1006,19 @@ cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
 }  // namespace hx
 
 // Every (equation, factor source, n_col) at order 7 with element-local x and
-// 16-byte aligned x / y, and the fused lattice gather (+ CG update) for the
+// 16-byte aligned x / y and fields, and the fused lattice gather (+ CG update) for the
 // Poisson trilinear / trilinear-partial sources; cudaErrorNotSupported otherwise.
 extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
   using namespace hx::mma;
   if (a->order != 7) return cudaErrorNotSupported;
   if (((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->y)) & (a->gather ? 7u : 15u)) != 0)
     return cudaErrorNotSupported;
+  // per-node fields: double2 loads and 16-byte bulk copies
+  const uintptr_t fields = reinterpret_cast<uintptr_t>(a->lam0) | reinterpret_cast<uintptr_t>(a->lam1) |
+                           reinterpret_cast<uintptr_t>(a->lam2) | reinterpret_cast<uintptr_t>(a->lam3) |
+                           reinterpret_cast<uintptr_t>(a->lam_geo) | reinterpret_cast<uintptr_t>(a->g) |
+                           reinterpret_cast<uintptr_t>(a->gwj);
+  if ((fields & 15u) != 0) return cudaErrorNotSupported;
   const bool helm = a->equation == HX_HELMHOLTZ;
   if (a->gather && (helm || (a->factor_source != HX_TRILINEAR && a->factor_source != HX_TRILINEAR_PARTIAL)))
     return cudaErrorNotSupported;  // the lattice gather is built for the trilinear Poisson sources

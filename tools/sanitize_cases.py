@@ -15,8 +15,8 @@ compute-sanitizer is closed on the GPU pool, so:
   reproduce the normal build's outputs bit for bit (--dump / --compare).
 
 ~64 elements per case.  Covers
-the N=7 kernels (DMMA ax8m n_col 1 / 3 (ax8m3) / fused lattice gather + CG
-update, ax8s, ax8c3), the order-generic role-table kernels (axn_r) at
+the N=7 kernels (DMMA ax8m n_col 1 / 3 (ax8m3, CTA3) with 0 / 1 / 2 staged
+coefficient fields / fused lattice gather + CG update, ax8s, ax8c3), the order-generic role-table kernels (axn_r) at
 n1 = 4, 7, 11, the slice kernel, the element-per-thread kernel, the j-plane
 kernel (orders 2, 3), the setup
 kernels and the BP5 gather / scatter (scatter_band32_kernel) / mask / dot /
@@ -73,12 +73,15 @@ def guard_operator(op):
             setattr(op, name, guarded(t.contiguous(), "read"))
 
 
-def case(order, dims, eq, src, n_col, kernel):
+def case(order, dims, eq, src, n_col, kernel, fields="lam0"):
     mesh = hx.box_mesh(*dims, order, perturbation=0.0 if src == "parallelepiped" else 0.12, seed=order)
     verts = mesh.vertices @ SHEAR.T if src == "parallelepiped" else mesh.vertices
     E, n3 = len(verts), (order + 1) ** 3
     rng = np.random.default_rng(order + n_col)
-    kw = {"lam0": rng.uniform(0.5, 2.0, (E, n3)), "lam1": 0.7} if eq == "helmholtz" else {}
+    kw = {}
+    if eq == "helmholtz":  # fields: which coefficients are (E, n1^3) fields (the DMMA kernel stages them)
+        kw = {"lam0": rng.uniform(0.5, 2.0, (E, n3)) if fields in ("lam0", "both") else 1.3,
+              "lam1": rng.uniform(0.5, 2.0, (E, n3)) if fields == "both" else 0.7}
     op = hx.LocalOperator(hx.KernelSpec(eq, n_col, src, order), torch.as_tensor(verts, device=DEV),
                           hx.SpectralBasis.build(order), **kw)
     op.kernel = kernel
@@ -88,7 +91,7 @@ def case(order, dims, eq, src, n_col, kernel):
     yd = guarded(torch.zeros_like(xd), "write")
     op.apply_(xd, yd)
     torch.cuda.synchronize()
-    tag = f"N={order} {eq} {src} n_col={n_col} kernel={kernel}"
+    tag = f"N={order} {eq} {src} n_col={n_col} kernel={kernel}" + ("" if fields == "lam0" else f" fields={fields}")
     check_guards(tag)
     y = yd.cpu().numpy()
     assert np.isfinite(y).all(), f"{tag}: non-finite output (out-of-bounds read of a NaN guard?)"
@@ -111,6 +114,10 @@ def main():
             for n_col in (1, 3):
                 case(7, (4, 4, 4), eq, src, n_col, kernel)
                 n += 1
+                if kernel == 4 and eq == "helmholtz":  # staged coefficient fields: both / none
+                    for fields in ("both", "none"):
+                        case(7, (4, 4, 4), eq, src, n_col, kernel, fields)
+                        n += 1
     # order-generic role-table kernels (axn_r) at n1 = 4, 7, 11; slice kernel; element per thread
     for order in (3, 6, 10):
         for src in ("trilinear", "stored", "parallelepiped"):
