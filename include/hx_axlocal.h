@@ -103,7 +103,10 @@ typedef struct {
                              2 = fast kernel (specialised N=7 ax8s / ax8c3, else order-generic);
                              3 = element-per-thread kernel (orders 1, 2 only);
                              4 = DMMA kernel (order 7 only: r/s contractions on
-                                 mma.sync m8n8k4 f64, ax_mma.cu) */
+                                 mma.sync m8n8k4 f64, ax_mma.cu; the kernel-0
+                                 choice at order 7 for every source but stored);
+                             5 = j-plane kernel (orders 2, 3: one thread per
+                                 j-plane, s direction by warp shuffles, ax_plane.cu) */
   int32_t reserved;       /* must be 0: nonzero values select experimental kernel
                              variants for the A/B tools and are rejected
                              (HX_ERR_INVALID) unless HX_TUNING=1 is set */
