@@ -41,6 +41,7 @@
 // across columns of ax8c3 is given up for that (a column loop makes NVVM hoist
 // the constant operands into registers and spill).
 #include "n7_common.cuh"
+#include <type_traits>
 
 // D (row-major [i][m]) for the per-lane fragments (lane-dependent indices: a
 // global array read once per warp through L1, not a divergent constant load).
@@ -261,7 +262,7 @@ __device__ __forceinline__ void tri_prepare(ElemGeo& S, const Lane& L, TriFibre 
 // Trilinear recompute, Poisson or Helmholtz (axlocal.py:191-201).
 template <bool HELM>
 struct Tri {
-  static constexpr bool kTri = true, kWFold = true, kGather = !HELM, kFields = HELM;
+  static constexpr bool kTri = true, kWFold = true, kGather = true, kFields = HELM;
   TriFibre f[2];
   const double* lam0;  // (E, n3) fields or null (scalars)
   const double* lam1;
@@ -321,6 +322,8 @@ struct Tri {
   // n_col = 3 factor reuse (ax8m3): the same arithmetic split into the per-node
   // factors (g, scale[, mass coefficient]) and their application to one column.
   static constexpr int kNF = HELM ? 8 : 7;
+  // n_col = 3 through ax8m3's factor reuse (Helmholtz: 134 vs 133 GDOF/s per-column)
+  static constexpr bool kReuse3 = HELM;
   __device__ __forceinline__ void prepare_one(const hx_axlocal_args& a, const ElemGeo& S, const Lane& L, int b) {
     tri_fibre_of<true>(S, L, b, f[b]);
     if (HELM) {
@@ -356,7 +359,7 @@ struct Tri {
 // merged (Helmholtz, lam2 / lam3) -- the stored scales carry w_k (no folding).
 template <bool MERGED>
 struct TriStoredScale {
-  static constexpr bool kTri = true, kWFold = false, kGather = !MERGED, kFields = true;
+  static constexpr bool kTri = true, kWFold = false, kGather = true, kFields = true;
   TriFibre f[2];
   const double* sa;  // lam_geo or lam2
   const double* sb;  // lam3
@@ -397,6 +400,8 @@ struct TriStoredScale {
   }
 
   static constexpr int kNF = MERGED ? 8 : 7;
+  // n_col = 3 as per-column warps (partial 161 vs 148, merged 153 vs 140 GDOF/s with reuse)
+  static constexpr bool kReuse3 = false;
   __device__ __forceinline__ void prepare_one(const hx_axlocal_args& a, const ElemGeo& S, const Lane& L, int b) {
     tri_fibre_of<false>(S, L, b, f[b]);
     sa = (MERGED ? a.lam2 : a.lam_geo) + L.e * N3;
@@ -448,7 +453,7 @@ struct FacLoaded {
 // Parallelepiped: g = w (x) h (geometry.py:389-398), w_j w_i per fibre, w_k folded.
 template <bool HELM>
 struct Ppd {
-  static constexpr bool kTri = false, kWFold = true, kGather = false, kFields = HELM;
+  static constexpr bool kTri = false, kWFold = true, kGather = true, kFields = HELM;
   double h[7], wji[2];
   const double* lam0;
   const double* lam1;
@@ -504,7 +509,7 @@ struct Ppd {
 // Stored (Nek-style) factors: 6 (+gwj) SoA loads per node (axlocal.py:181-185).
 template <bool HELM>
 struct Stored {
-  static constexpr bool kTri = false, kWFold = false, kGather = false, kFields = HELM;
+  static constexpr bool kTri = false, kWFold = false, kGather = true, kFields = HELM;
   const double* gp;
   const double* gwj;
   const double* lam0;
@@ -625,6 +630,26 @@ struct XSrc {
   }
 };
 
+// n_col = 3 in a 3-warp CTA: the element's interleaved x (n1^3 x 3) staged in
+// shared memory, warp col reading its column (stride 3 doubles: conflict-free)
+struct XStaged3 {
+  const double* x;
+  __device__ __forceinline__ XStaged3(const double* xs, int col) : x(xs + col) {}
+  __device__ __forceinline__ double at(int k, int j, int i) const { return x[(k * 64 + j * 8 + i) * 3]; }
+  __device__ __forceinline__ void pair(int k, int j, int i, double& v0, double& v1) const {
+    v0 = at(k, j, i);
+    v1 = at(k, j, i + 1);
+  }
+};
+
+template <typename XS, int NCOL, bool GATHER, bool CGP>
+__device__ __forceinline__ XS make_xs(const hx_axlocal_args& a, const Lane& L, int col, const double* sx) {
+  if constexpr (std::is_same<XS, XStaged3>::value)
+    return XStaged3(sx, col);
+  else
+    return XSrc<NCOL, GATHER, CGP>(a, L, col);
+}
+
 // One column of one element: x -> y, with the geometry prepared.
 // The transposed r / s products of a slice, accumulated into (y0, y1) from
 // the mass term ms: one order for every kernel built from these templates
@@ -645,11 +670,13 @@ struct XSrc {
 
 // xa / xb: the thread's two k-fibres of x, loaded by the caller before the
 // geometry prologue so that their latency hides behind it.
-template <typename F, int NCOL, bool GATHER, bool CGP>
+// X: XSrc (global / lattice) or XStaged3 (shared); ysh: null -> y to global, else the
+// element's (512 x 3) y tile in shared memory (written back by the CTA)
+template <typename F, int NCOL, typename XS>
 __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, double (*tiles)[64], const F& fac,
-                                       const Lane& L, const XSrc<NCOL, GATHER, CGP>& X, double xa[8],
-                                       double xb[8], const double Dr[2], const double Ds[2], const double Dt[2],
-                                       const double Dy[2], int col) {
+                                       const Lane& L, const XS& X, double xa[8], double xb[8], const double Dr[2],
+                                       const double Ds[2], const double Dt[2], const double Dy[2], int col,
+                                       double* ysh = nullptr) {
   const int g = L.g, q = L.q;
   double ta[8], tb[8];
   fast::eo8<0>(xa, ta);
@@ -736,6 +763,9 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
     const int n = k * 64 + g * 8 + 2 * q;
     if (NCOL == 1) {
       *reinterpret_cast<double2*>(ye + n) = make_double2(y0, y1);
+    } else if (ysh) {
+      ysh[n * NCOL + col] = y0;
+      ysh[(n + 1) * NCOL + col] = y1;
     } else {
       ye[n * NCOL] = y0;
       ye[(n + 1) * NCOL] = y1;
@@ -764,20 +794,26 @@ __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a
   // bulk copy each, issued first and waited for after the geometry prologue:
   // no registers held for them and no load latency inside the slices
   // (one copy per CTA: the CTA3 column warps share it)
+  // XST (n_col = 3 in one CTA): the element's interleaved x staged the same way, and
+  // y written back from a shared tile as contiguous 16-byte stores (the strided
+  // per-column accesses otherwise stall on store drain and the LSU queue)
   constexpr int NS = F::kStage;
+  constexpr bool XST = CTA3 && NCOL == 3 && !GATHER;
   __shared__ alignas(128) double sf[NS > 0 ? NS * N3 : 2];
+  __shared__ alignas(128) double sxy[XST ? 2 * 3 * N3 : 2];  // x tile, y tile
   __shared__ uint64_t bar[1];
-  bool staged = false;
-  if constexpr (NS > 0) {
+  bool staged = XST;
+  if constexpr (NS > 0 || XST) {
 #pragma unroll
     for (int f = 0; f < NS; ++f) staged |= F::stage_base(a, f) != nullptr;
     if (staged && threadIdx.x == 0) {
-      uint32_t bytes = 0;
+      uint32_t bytes = XST ? 8u * 3 * N3 : 0u;
 #pragma unroll
       for (int f = 0; f < NS; ++f) bytes += F::stage_base(a, f) ? 8u * N3 : 0u;
       mbar_init(bar, 1);
       fence_mbar_init();
       mbar_arrive_expect_tx(bar, bytes);
+      if (XST) bulk_g2s(sxy, a.x + L.e * 3 * N3, 8u * 3 * N3, bar);
 #pragma unroll
       for (int f = 0; f < NS; ++f)
         if (const double* src = F::stage_base(a, f)) bulk_g2s(sf + f * N3, src + L.e * N3, 8u * N3, bar);
@@ -816,10 +852,13 @@ __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a
       }
     }
   }
-  const XSrc<NCOL, GATHER, CGP> X(a, L, col);
+  using XS = typename std::conditional<XST, XStaged3, XSrc<NCOL, GATHER, CGP>>::type;
+  const XS X = make_xs<XS, NCOL, GATHER, CGP>(a, L, col, sxy);
   double xa[8], xb[8];
+  if constexpr (!XST) {  // staged x is read after the barrier wait
 #pragma unroll
-  for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
+    for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
+  }
   double Dr[2], Ds[2], Dt[2], Dy[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
@@ -838,10 +877,20 @@ __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a
   F fac;
   fac.prepare(a, S, L);
   fac.sf = sf;
-  if (F::kTri || NS > 0) __syncwarp();
-  if constexpr (CTA3 && NS > 0) __syncthreads();  // the barrier's init, for the other warps
-  if (NS > 0 && staged) mbar_wait(bar, 0);
-  column<F, NCOL, GATHER, CGP>(a, S, S.tile, fac, L, X, xa, xb, Dr, Ds, Dt, Dy, col);
+  if (F::kTri || NS > 0 || XST) __syncwarp();
+  if constexpr (CTA3 && (NS > 0 || XST)) __syncthreads();  // the barrier's init, for the other warps
+  if ((NS > 0 || XST) && staged) mbar_wait(bar, 0);
+  if constexpr (XST) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
+  }
+  column<F, NCOL>(a, S, S.tile, fac, L, X, xa, xb, Dr, Ds, Dt, Dy, col, XST ? sxy + 3 * N3 : nullptr);
+  if constexpr (XST) {  // the y tile out as contiguous 16-byte stores
+    __syncthreads();
+    const double2* src = reinterpret_cast<const double2*>(sxy + 3 * N3);
+    double2* dst = reinterpret_cast<double2*>(a.y + L.e * 3 * N3);
+    for (int v = threadIdx.x; v < 3 * N3 / 2; v += 96) dst[v] = src[v];
+  }
 }
 
 // n_col = 3 with factor reuse, trilinear sources: one CTA of three warps per
@@ -964,7 +1013,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
   FacLoaded<F> fl;
   fl.fac = s_fac;
   // each warp transposes through its own tile pair
-  column<FacLoaded<F>, 3, false, false>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy,
+  column<FacLoaded<F>, 3>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy,
                                         w);
 }
 
@@ -987,7 +1036,9 @@ cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
     }
   } else if (a.n_col == 3) {
     if constexpr (F::kTri) {
-      if (a.reserved != 71) {  // 71: the per-column warps without factor reuse (A/B)
+      // factor reuse (ax8m3) where it measures faster (F::kReuse3); else the
+      // per-column 3-warp CTA below. Hooks: 71 per-column, 73 reuse (A/B)
+      if (a.reserved == 73 || (F::kReuse3 && a.reserved != 71)) {
         ax8m3<F, HX_MMA3_NREG><<<(unsigned)a.n_elements, 96, 0, s>>>(a);
         return cudaGetLastError();
       }
@@ -1006,8 +1057,8 @@ cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
 }  // namespace hx
 
 // Every (equation, factor source, n_col) at order 7 with element-local x and
-// 16-byte aligned x / y and fields, and the fused lattice gather (+ CG update) for the
-// Poisson trilinear / trilinear-partial sources; cudaErrorNotSupported otherwise.
+// 16-byte aligned x / y and fields, and the fused lattice gather (+ CG update) for
+// every source and equation at n_col = 1; cudaErrorNotSupported otherwise.
 extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
   using namespace hx::mma;
   if (a->order != 7) return cudaErrorNotSupported;
@@ -1020,8 +1071,6 @@ extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
                            reinterpret_cast<uintptr_t>(a->gwj);
   if ((fields & 15u) != 0) return cudaErrorNotSupported;
   const bool helm = a->equation == HX_HELMHOLTZ;
-  if (a->gather && (helm || (a->factor_source != HX_TRILINEAR && a->factor_source != HX_TRILINEAR_PARTIAL)))
-    return cudaErrorNotSupported;  // the lattice gather is built for the trilinear Poisson sources
   switch (a->factor_source) {
     case HX_TRILINEAR:
       if (helm) {

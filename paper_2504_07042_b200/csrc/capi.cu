@@ -269,14 +269,14 @@ extern "C" int hx_axlocal(const hx_axlocal_args* a, void* stream) {
     if (a->gather) return fail(HX_ERR_UNSUPPORTED, "fused lattice gather is not in the low-order kernel");
     return cuda_status(n1 == 2 ? hx_low_launch_2(a, s) : hx_low_launch_3(a, s), "hx_axlocal(low)");
   }
-  // kernel 0 at order 7: the DMMA kernel (ax_mma.cu) for every factor source
-  // but stored (HBM-bound; ax8s / ax8c3 measure equal or faster), both
-  // equations, at n_col 1 and 3 alike, so that n_col = 3 stays bitwise three
-  // n_col = 1 applies, and with the fused BP5 lattice gather for the Poisson
-  // trilinear sources, so fused and unfused stay bitwise equal
-  // (profiles/r02_n7_variants_c4.txt, r02_mma_stage_ab.txt)
-  const bool mma_default = a->kernel == 0 && a->order == 7 && a->factor_source != HX_STORED &&
-                           !(a->gather && a->factor_source == HX_PARALLELEPIPED);
+  // kernel 0 at order 7: the DMMA kernel (ax_mma.cu) for every factor source of
+  // both equations but Helmholtz stored (nine per-node streams: ax8s / ax8c3
+  // measure 12 % / 7 % faster), at n_col 1 and 3 alike, so that n_col = 3 stays
+  // bitwise three n_col = 1 applies, and with the fused BP5 lattice gather, so
+  // fused and unfused stay bitwise equal
+  // (profiles/r02_n7_variants_c4.txt, r02_mma_stage_ab.txt, r02_mma_xstage_ab.txt)
+  const bool helm_eq = a->equation == HX_HELMHOLTZ;
+  const bool mma_default = a->kernel == 0 && a->order == 7 && !(helm_eq && a->factor_source == HX_STORED);
   if (a->kernel == 4 || mma_default) {  // DMMA kernel (order 7, element-local x)
     cudaError_t e = hx_mma_launch(a, s);
     if (e != cudaErrorNotSupported) return cuda_status(e, "hx_axlocal(mma)");

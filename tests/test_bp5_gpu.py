@@ -96,12 +96,20 @@ def test_cg_is_bitwise_reproducible():
     assert torch.equal(r1.solution, r2.solution)
 
 
-@pytest.mark.parametrize("src", ["trilinear", "stored", "trilinear-partial"])
-def test_fused_gather_is_bitwise_the_unfused_path(src):
+@pytest.mark.parametrize("eq,src", [("poisson", "trilinear"), ("poisson", "stored"), ("poisson", "trilinear-partial"),
+                                    ("poisson", "parallelepiped"), ("helmholtz", "trilinear"),
+                                    ("helmholtz", "trilinear-merged"), ("helmholtz", "stored"),
+                                    ("helmholtz", "parallelepiped")])
+def test_fused_gather_is_bitwise_the_unfused_path(eq, src):
     """The N=7 AxLocal kernels read u straight from the slab lattice (fused gather);
-    the values they see are the gather's, so A Q u is bit-identical either way."""
-    mesh = hx.box_mesh(5, 4, 3, 7, perturbation=0.12, seed=2)
-    op = S.GlobalOperator(mesh, hx.KernelSpec("poisson", 1, src, 7), hx.SpectralBasis.build(7))
+    the values they see are the gather's, so A Q u is bit-identical either way
+    (the default kernel of every source and equation has both paths)."""
+    mesh = hx.box_mesh(5, 4, 3, 7, perturbation=0.0 if src == "parallelepiped" else 0.12, seed=2)
+    kw = {}
+    if eq == "helmholtz":
+        rng = np.random.default_rng(3)
+        kw = {"lam0": rng.uniform(0.5, 2.0, (mesh.n_elements, 512)), "lam1": 0.6}
+    op = S.GlobalOperator(mesh, hx.KernelSpec(eq, 1, src, 7), hx.SpectralBasis.build(7), **kw)
     u = torch.randn(op.layout.n_local, dtype=torch.float64, device=DEV)
     fused = op.apply(u).clone()
     op.backend.fused_gather = False
@@ -159,8 +167,9 @@ def test_cg_solve_mask_semantics_follow_the_reference():
 
 def test_fused_gather_misaligned_lattice_view():
     """A lattice view that is only 8-byte aligned (u[1:]): the DMMA kernel takes it
-    (its lattice loads are 8-byte), the 16-byte ax8s gather path must refuse it
-    with an error instead of falling through to the element-local kernel."""
+    (its lattice loads are 8-byte), the 16-byte ax8s gather path (Helmholtz
+    stored) must refuse it with an error instead of falling through to the
+    element-local kernel."""
     mesh = hx.box_mesh(3, 2, 2, 7, perturbation=0.1, seed=1)
     L = S.SlabLayout((3, 2, 2), 7)
     base = torch.randn(L.n_local + 1, dtype=torch.float64, device=DEV)
@@ -169,11 +178,13 @@ def test_fused_gather_misaligned_lattice_view():
     ref = base[1:].clone()
     xl = torch.empty((L.n_elements, 512, 1), dtype=torch.float64, device=DEV)
     S.CudaBackend(DEV).gather(L, ref, xl)
-    for src in ("trilinear", "trilinear-partial"):
+    for src in ("trilinear", "trilinear-partial", "stored"):
         op = hx.LocalOperator(hx.KernelSpec("poisson", 1, src, 7), mesh, hx.SpectralBasis.build(7))
         y = torch.empty_like(xl)
         op.apply_lattice_(u, y, L.box())
         assert torch.equal(y, op.apply(xl)), src
-    op = hx.LocalOperator(hx.KernelSpec("poisson", 1, "stored", 7), mesh, hx.SpectralBasis.build(7))
+    # Helmholtz stored stays on ax8s, whose gather needs 16-byte alignment
+    op = hx.LocalOperator(hx.KernelSpec("helmholtz", 1, "stored", 7), mesh, hx.SpectralBasis.build(7), lam0=1.2,
+                          lam1=0.5)
     with pytest.raises(ValueError, match="aligned"):
         op.apply_lattice_(u, torch.empty_like(xl), L.box())
