@@ -104,7 +104,8 @@ typedef struct {
                              3 = element-per-thread kernel (orders 1, 2 only);
                              4 = DMMA kernel (order 7 only: r/s contractions on
                                  mma.sync m8n8k4 f64, ax_mma.cu; the kernel-0
-                                 choice at order 7 for every source but stored);
+                                 choice at order 7 for every source and equation
+                                 but Helmholtz stored);
                              5 = j-plane kernel (orders 2, 3: one thread per
                                  j-plane, s direction by warp shuffles, ax_plane.cu) */
   int32_t reserved;       /* must be 0: nonzero values select experimental kernel
