@@ -179,7 +179,16 @@ __device__ __forceinline__ AxisCopies32 axis_copies32(int g, int n, int ne, int 
   return a;
 }
 
-__global__ void __launch_bounds__(256, 8) scatter_band32_kernel(Box b, const double* __restrict__ yl,
+// rows in flight per thread / blocks per SM: deeper unrolling (8, 16 rows at 4 or 2
+// blocks per SM) made the C5 solve 15 % slower (profiles/r02_scatter_ab.txt)
+#ifndef HX_SCATTER_UNROLL
+#define HX_SCATTER_UNROLL 4
+#endif
+#ifndef HX_SCATTER_MINB
+#define HX_SCATTER_MINB 8
+#endif
+constexpr int kScatterUnroll = HX_SCATTER_UNROLL;
+__global__ void __launch_bounds__(256, HX_SCATTER_MINB) scatter_band32_kernel(Box b, const double* __restrict__ yl,
                                                                 double* __restrict__ v, const double* __restrict__ p,
                                                                 int64_t n_owned, double* __restrict__ partial,
                                                                 int do_mask) {
@@ -199,7 +208,7 @@ __global__ void __launch_bounds__(256, 8) scatter_band32_kernel(Box b, const dou
   for (int gx = threadIdx.x; gx < nx; gx += blockDim.x) {
     const AxisCopies32 ax = axis_copies32(gx, n, b.ex, n3, 1);
     const bool col_boundary = plane_boundary || gx == 0 || gx == nx - 1;
-#pragma unroll 4
+#pragma unroll kScatterUnroll
     for (int gy = gy0; gy < gy1; ++gy) {
       const AxisCopies32 ay = axis_copies32(gy, n, b.ey, ex_n3, n1);
       double acc = 0.0;
