@@ -29,7 +29,12 @@ import paper_2504_07042_b200 as hx  # noqa: E402
 from oracle import hosfem_oracle as O  # noqa: E402
 from paper_2504_07042_b200.workload import workload_count  # noqa: E402
 
-FP64, HBM = 37.0e12, 6.5501e12
+FP64 = 37.0e12  # measured DFMA / DMMA peak (profiles/r01_ubench_fp64.txt)
+try:  # the driver-measured copy bandwidth
+    HBM = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9
+except Exception:
+    HBM = 6.4574e12
 ORDER = 7
 N3 = (ORDER + 1) ** 3
 
@@ -82,7 +87,11 @@ def run(config, verts, variants, reps, dev, rows):
     yd = torch.empty_like(xd)
     basis = hx.SpectralBasis.build(ORDER)
     for source, equation in variants:
-        kw = {"lam0": 1.3, "lam1": 0.4} if equation == "helmholtz" else {}
+        # Helmholtz with coefficient FIELDS: the work model charges two per-node
+        # coefficient reads, which scalar coefficients would never make
+        rng = np.random.default_rng(7)
+        kw = ({"lam0": rng.uniform(0.5, 2.0, (E, N3)), "lam1": rng.uniform(0.5, 2.0, (E, N3))}
+              if equation == "helmholtz" else {})
         spec = hx.KernelSpec(equation, 1, source, ORDER)
         op = hx.LocalOperator(spec, torch.as_tensor(verts, device=dev), basis, device=dev, **kw)
         t_gpu = gpu_time(op, xd, yd, reps)
