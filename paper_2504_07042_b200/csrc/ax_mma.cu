@@ -322,8 +322,9 @@ struct Tri {
   // n_col = 3 factor reuse (ax8m3): the same arithmetic split into the per-node
   // factors (g, scale[, mass coefficient]) and their application to one column.
   static constexpr int kNF = HELM ? 8 : 7;
-  // n_col = 3 through ax8m3's factor reuse (Helmholtz: 134 vs 133 GDOF/s per-column)
-  static constexpr bool kReuse3 = HELM;
+  // n_col = 3 through ax8m3's factor reuse (Poisson 159 vs 148, Helmholtz 133 vs 128
+  // GDOF/s per-column; profiles/r02_mma3_xstage_ab.txt)
+  static constexpr bool kReuse3 = true;
   __device__ __forceinline__ void prepare_one(const hx_axlocal_args& a, const ElemGeo& S, const Lane& L, int b) {
     tri_fibre_of<true>(S, L, b, f[b]);
     if (HELM) {
@@ -400,8 +401,9 @@ struct TriStoredScale {
   }
 
   static constexpr int kNF = MERGED ? 8 : 7;
-  // n_col = 3 as per-column warps (partial 161 vs 148, merged 153 vs 140 GDOF/s with reuse)
-  static constexpr bool kReuse3 = false;
+  // n_col = 3: partial through ax8m3's factor reuse (161 vs 151 GDOF/s per-column),
+  // merged as per-column warps (148 vs 143; profiles/r02_mma3_xstage_ab.txt)
+  static constexpr bool kReuse3 = !MERGED;
   __device__ __forceinline__ void prepare_one(const hx_axlocal_args& a, const ElemGeo& S, const Lane& L, int b) {
     tri_fibre_of<false>(S, L, b, f[b]);
     sa = (MERGED ? a.lam2 : a.lam_geo) + L.e * N3;
@@ -670,8 +672,10 @@ __device__ __forceinline__ XS make_xs(const hx_axlocal_args& a, const Lane& L, i
 
 // xa / xb: the thread's two k-fibres of x, loaded by the caller before the
 // geometry prologue so that their latency hides behind it.
-// X: XSrc (global / lattice) or XStaged3 (shared); ysh: null -> y to global, else the
-// element's (512 x 3) y tile in shared memory (written back by the CTA)
+// X: XSrc (global / lattice) or XStaged3 (shared); ysh: null -> y to global, kYRegs ->
+// y returned in xa / xb, else the element's (512 x 3) y tile in shared memory
+// (written back by the CTA)
+__device__ double* const kYRegs = reinterpret_cast<double*>(1);
 template <typename F, int NCOL, typename XS>
 __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, double (*tiles)[64], const F& fac,
                                        const Lane& L, const XS& X, double xa[8], double xb[8], const double Dr[2],
@@ -761,7 +765,10 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
       y1 = xb[k] + yb[k];
     }
     const int n = k * 64 + g * 8 + 2 * q;
-    if (NCOL == 1) {
+    if (ysh == kYRegs) {  // returned in xa / xb, stored by the caller
+      xa[k] = y0;
+      xb[k] = y1;
+    } else if (NCOL == 1) {
       *reinterpret_cast<double2*>(ye + n) = make_double2(y0, y1);
     } else if (ysh) {
       ysh[n * NCOL + col] = y0;
@@ -903,33 +910,33 @@ __global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a
 template <typename F, int NREG>
 __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args a) {
   constexpr int MINB = 65536 / (32 * NREG);
+  constexpr int NS = F::kStage;
   __shared__ ElemGeo S;
   __shared__ double s_tile[2][2][64];  // warps 1, 2 (warp 0 uses S.tile)
-  __shared__ double2 s_fac[8][F::kNF][32];
+  __shared__ uint64_t bar[1];
+  // dynamic: the per-node factors [8][kNF][32] (then the y tile), the element's
+  // interleaved x (512 x 3), the per-node fields of the factor phase
+  extern __shared__ __align__(128) double dsm[];
+  double2(*s_fac)[F::kNF][32] = reinterpret_cast<double2(*)[F::kNF][32]>(dsm);
+  double* const sx = dsm + 2 * 8 * F::kNF * 32;
+  double* const sf = sx + 3 * N3;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Lane L;
   L.e = blockIdx.x;
   L.g = lane >> 2;
   L.q = lane & 3;
-  // the per-node fields of the factor phase, staged as in ax8m
-  constexpr int NS = F::kStage;
-  __shared__ alignas(128) double sf[NS > 0 ? NS * N3 : 2];
-  __shared__ uint64_t bar[1];
-  bool staged = false;
-  if constexpr (NS > 0) {
+  // x and the fields staged as in ax8m (one barrier for all copies)
+  if (threadIdx.x == 0) {
+    uint32_t bytes = 8u * 3 * N3;
 #pragma unroll
-    for (int f = 0; f < NS; ++f) staged |= F::stage_base(a, f) != nullptr;
-    if (staged && threadIdx.x == 0) {
-      uint32_t bytes = 0;
+    for (int f = 0; f < NS; ++f) bytes += F::stage_base(a, f) ? 8u * N3 : 0u;
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(sx, a.x + L.e * 3 * N3, 8u * 3 * N3, bar);
 #pragma unroll
-      for (int f = 0; f < NS; ++f) bytes += F::stage_base(a, f) ? 8u * N3 : 0u;
-      mbar_init(bar, 1);
-      fence_mbar_init();
-      mbar_arrive_expect_tx(bar, bytes);
-#pragma unroll
-      for (int f = 0; f < NS; ++f)
-        if (const double* src = F::stage_base(a, f)) bulk_g2s(sf + f * N3, src + L.e * N3, 8u * N3, bar);
-    }
+    for (int f = 0; f < NS; ++f)
+      if (const double* src = F::stage_base(a, f)) bulk_g2s(sf + f * N3, src + L.e * N3, 8u * N3, bar);
   }
   if (threadIdx.x < 2) {
     const int64_t ahead = L.e + (int64_t)148 * MINB * HX_MMA_AHEAD_WAVES4 / 4 / 3;
@@ -946,10 +953,8 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
       }
     }
   }
-  const XSrc<3, false, false> X(a, L, w);
+  const XStaged3 X(sx, w);
   double xa[8], xb[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
   double Dr[2], Ds[2], Dt[2], Dy[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
@@ -971,7 +976,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
       tri_tables(S, lane & 7, 4 + (lane >> 3));
     }
     __syncthreads();
-    if (NS > 0 && staged && w < 2) mbar_wait(bar, 0);
+    if (w < 2) mbar_wait(bar, 0);  // the fields (and x)
     if (w < 2) {
       double* dst = reinterpret_cast<double*>(&s_fac[0][0][lane]) + w;
 #define HX_FAC(K)                                                        \
@@ -993,7 +998,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
       tri_tables(S, lane & 7, 4 + (lane >> 3));
     }
     __syncthreads();
-    if (NS > 0 && staged && w < 2) mbar_wait(bar, 0);
+    if (w < 2) mbar_wait(bar, 0);  // the fields (and x)
 #define HX_FAC(K)                                                        \
   {                                                                      \
     double v0[F::kNF], v1[F::kNF];                                       \
@@ -1010,11 +1015,34 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
 #endif
   }
   __syncthreads();
+  if (w == 2) mbar_wait(bar, 0);  // x
+#pragma unroll
+  for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
   FacLoaded<F> fl;
   fl.fac = s_fac;
-  // each warp transposes through its own tile pair
-  column<FacLoaded<F>, 3>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy,
-                                        w);
+  // each warp transposes through its own tile pair; y comes back in xa / xb
+  column<FacLoaded<F>, 3>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy, w,
+                          kYRegs);
+  // the y tile in the factor buffer once every warp is done with the factors,
+  // then out as contiguous 16-byte stores
+  __syncthreads();
+  double* const sy = dsm;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int n = k * 64 + L.g * 8 + 2 * L.q;
+    sy[n * 3 + w] = xa[k];
+    sy[(n + 1) * 3 + w] = xb[k];
+  }
+  __syncthreads();
+  const double2* src = reinterpret_cast<const double2*>(sy);
+  double2* dst = reinterpret_cast<double2*>(a.y + L.e * 3 * N3);
+  for (int v = threadIdx.x; v < 3 * N3 / 2; v += 96) dst[v] = src[v];
+}
+
+// dynamic shared memory of ax8m3<F>: factors (>= the y tile), x, staged fields
+template <typename F>
+constexpr size_t ax8m3_dsmem() {
+  return sizeof(double) * (2 * 8 * F::kNF * 32 + 3 * N3 + F::kStage * N3);
 }
 
 
@@ -1039,7 +1067,15 @@ cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
       // factor reuse (ax8m3) where it measures faster (F::kReuse3); else the
       // per-column 3-warp CTA below. Hooks: 71 per-column, 73 reuse (A/B)
       if (a.reserved == 73 || (F::kReuse3 && a.reserved != 71)) {
-        ax8m3<F, HX_MMA3_NREG><<<(unsigned)a.n_elements, 96, 0, s>>>(a);
+        constexpr size_t dsm = ax8m3_dsmem<F>();
+        static bool attr = false;  // the opt-in above 48 KB, once per instantiation
+        if (!attr) {
+          const cudaError_t e = cudaFuncSetAttribute(ax8m3<F, HX_MMA3_NREG>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+          if (e != cudaSuccess) return e;
+          attr = true;
+        }
+        ax8m3<F, HX_MMA3_NREG><<<(unsigned)a.n_elements, 96, dsm, s>>>(a);
         return cudaGetLastError();
       }
     }
