@@ -785,7 +785,12 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
 // CTA3: the element's three column warps in one CTA (one SM, so the strided
 // column loads of x share L1 lines), else one CTA per (element, column).
 template <typename F, int NCOL, int NREG, bool GATHER = false, bool CGP = false, bool CTA3 = false>
-__global__ void __maxnreg__(NREG) ax8m(const __grid_constant__ hx_axlocal_args a) {
+#ifdef HX_MMA_LAUNCH_BOUNDS  // register budget as launch bounds instead of a cap (A/B: +0.2 %, within noise)
+__global__ void __launch_bounds__(CTA3 ? 96 : 32, 65536 / (32 * NREG) / (CTA3 ? 3 : 1))
+#else
+__global__ void __maxnreg__(NREG)
+#endif
+ax8m(const __grid_constant__ hx_axlocal_args a) {
   constexpr int MINB = 65536 / (32 * NREG);
   __shared__ ElemGeo S_[CTA3 ? NCOL : 1];
   const int lane = threadIdx.x & 31;
