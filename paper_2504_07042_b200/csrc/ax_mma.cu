@@ -1073,13 +1073,10 @@ cudaError_t launch(const hx_axlocal_args& a, cudaStream_t s) {
       // per-column 3-warp CTA below. Hooks: 71 per-column, 73 reuse (A/B)
       if (a.reserved == 73 || (F::kReuse3 && a.reserved != 71)) {
         constexpr size_t dsm = ax8m3_dsmem<F>();
-        static bool attr = false;  // the opt-in above 48 KB, once per instantiation
-        if (!attr) {
-          const cudaError_t e = cudaFuncSetAttribute(ax8m3<F, HX_MMA3_NREG>,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-          if (e != cudaSuccess) return e;
-          attr = true;
-        }
+        // the opt-in above 48 KB is per device: set it on every launch (~1 us host call)
+        const cudaError_t e = cudaFuncSetAttribute(ax8m3<F, HX_MMA3_NREG>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        if (e != cudaSuccess) return e;
         ax8m3<F, HX_MMA3_NREG><<<(unsigned)a.n_elements, 96, dsm, s>>>(a);
         return cudaGetLastError();
       }
