@@ -672,11 +672,11 @@ __device__ __forceinline__ XS make_xs(const hx_axlocal_args& a, const Lane& L, i
 
 // xa / xb: the thread's two k-fibres of x, loaded by the caller before the
 // geometry prologue so that their latency hides behind it.
-// X: XSrc (global / lattice) or XStaged3 (shared); ysh: null -> y to global, kYRegs ->
-// y returned in xa / xb, else the element's (512 x 3) y tile in shared memory
-// (written back by the CTA)
-__device__ double* const kYRegs = reinterpret_cast<double*>(1);
-template <typename F, int NCOL, typename XS>
+// X: XSrc (global / lattice) or XStaged3 (shared).  Where y goes (YOut): to
+// global memory, into the element's (512 x 3) y tile ysh in shared memory
+// (written back by the CTA), or back to the caller in xa / xb.
+enum class YOut { kGlobal, kTile, kRegs };
+template <typename F, int NCOL, typename XS, YOut YO = YOut::kGlobal>
 __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, double (*tiles)[64], const F& fac,
                                        const Lane& L, const XS& X, double xa[8], double xb[8], const double Dr[2],
                                        const double Ds[2], const double Dt[2], const double Dy[2], int col,
@@ -765,14 +765,14 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
       y1 = xb[k] + yb[k];
     }
     const int n = k * 64 + g * 8 + 2 * q;
-    if (ysh == kYRegs) {  // returned in xa / xb, stored by the caller
+    if constexpr (YO == YOut::kRegs) {
       xa[k] = y0;
       xb[k] = y1;
-    } else if (NCOL == 1) {
-      *reinterpret_cast<double2*>(ye + n) = make_double2(y0, y1);
-    } else if (ysh) {
+    } else if constexpr (YO == YOut::kTile) {
       ysh[n * NCOL + col] = y0;
       ysh[(n + 1) * NCOL + col] = y1;
+    } else if constexpr (NCOL == 1) {
+      *reinterpret_cast<double2*>(ye + n) = make_double2(y0, y1);
     } else {
       ye[n * NCOL] = y0;
       ye[(n + 1) * NCOL] = y1;
@@ -896,7 +896,8 @@ ax8m(const __grid_constant__ hx_axlocal_args a) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) X.pair(k, L.g, 2 * L.q, xa[k], xb[k]);
   }
-  column<F, NCOL>(a, S, S.tile, fac, L, X, xa, xb, Dr, Ds, Dt, Dy, col, XST ? sxy + 3 * N3 : nullptr);
+  column<F, NCOL, XS, XST ? YOut::kTile : YOut::kGlobal>(a, S, S.tile, fac, L, X, xa, xb, Dr, Ds, Dt, Dy, col,
+                                                        XST ? sxy + 3 * N3 : nullptr);
   if constexpr (XST) {  // the y tile out as contiguous 16-byte stores
     __syncthreads();
     const double2* src = reinterpret_cast<const double2*>(sxy + 3 * N3);
@@ -1026,8 +1027,8 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
   FacLoaded<F> fl;
   fl.fac = s_fac;
   // each warp transposes through its own tile pair; y comes back in xa / xb
-  column<FacLoaded<F>, 3>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds, Dt, Dy, w,
-                          kYRegs);
+  column<FacLoaded<F>, 3, XStaged3, YOut::kRegs>(a, S, w == 0 ? S.tile : s_tile[w - 1], fl, L, X, xa, xb, Dr, Ds,
+                                                 Dt, Dy, w);
   // the y tile in the factor buffer once every warp is done with the factors,
   // then out as contiguous 16-byte stores
   __syncthreads();
