@@ -1113,7 +1113,8 @@ extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
   switch (a->factor_source) {
     case HX_TRILINEAR:
       if (helm) {
-        // 232 registers: 114 GDOF/s vs 100 at 168 (still below ax8s, profiles/r02_mma_fields_ab.txt)
+        // 232 registers: +1.5 % with coefficient fields, -0.7 % with scalars; 184 / 200: -6 / -2 %
+        // (after the field staging; profiles/r02_mma_fields_ab.txt for the numbers before it)
         if (a->reserved == 65) return launch<Tri<true>, 232>(*a, s);
         return launch<Tri<true>>(*a, s);
       }
