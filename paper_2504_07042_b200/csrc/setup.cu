@@ -6,6 +6,7 @@
 // configuration they still take well under a second, where the reference's
 // numpy setup cannot allocate its temporaries.
 #include "hx_common.cuh"
+#include <cstdlib>
 
 namespace hx {
 namespace {
@@ -146,6 +147,85 @@ __global__ void stored_setup_kernel(int n1, int64_t E, const double* __restrict_
   }
 }
 
+// The same computation at a compile-time order (N1T points), the orders the
+// bench and the tests build most: unrolled loops, shift / mask node indices,
+// D from shared memory (its lane-dependent rows made the constant-bank loads of
+// the generic kernel serialize; 65 ms -> see profiles/r02_setup_ab.txt at C4).
+// Same operations in the same order as stored_setup_kernel.
+template <int N1T>
+__global__ void __launch_bounds__(256) stored_setup_kernel_ct(int64_t E, const double* __restrict__ verts,
+                                                             double* g_out, double* gwj_out, int64_t* first_bad) {
+  constexpr int n1 = N1T, n3 = n1 * n1 * n1;
+  __shared__ double s_xyz[3 * n3];
+  __shared__ double sD[n1 * n1];
+  const int64_t e = blockIdx.x;
+  const int od = off_d(n1), op = off_p(n1);
+  const double* xi = c_X + op;
+  for (int q = threadIdx.x; q < n1 * n1; q += blockDim.x) sD[q] = c_D[od + q];
+  double v[24];
+#pragma unroll
+  for (int q = 0; q < 24; ++q) v[q] = __ldg(verts + e * 24 + q);
+  for (int node = threadIdx.x; node < n3; node += blockDim.x) {
+    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s_xyz[c * n3 + node] = node_coord(v, xi, i, j, k, c);
+  }
+  __syncthreads();
+  for (int node = threadIdx.x; node < n3; node += blockDim.x) {
+    const int i = node % n1, j = (node / n1) % n1, k = node / (n1 * n1);
+    double jac[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double* X = s_xyz + c * n3;
+      double dr = 0.0, ds = 0.0, dt = 0.0;
+#pragma unroll
+      for (int n = 0; n < n1; ++n) {
+        dr = __dadd_rn(dr, __dmul_rn(sD[i * n1 + n], X[(k * n1 + j) * n1 + n]));
+        ds = __dadd_rn(ds, __dmul_rn(sD[j * n1 + n], X[(k * n1 + n) * n1 + i]));
+        dt = __dadd_rn(dt, __dmul_rn(sD[k * n1 + n], X[(n * n1 + j) * n1 + i]));
+      }
+      jac[c][0] = dr;
+      jac[c][1] = ds;
+      jac[c][2] = dt;
+    }
+    const double c0[3] = {jac[0][0], jac[1][0], jac[2][0]};
+    const double c1[3] = {jac[0][1], jac[1][1], jac[2][1]};
+    const double c2[3] = {jac[0][2], jac[1][2], jac[2][2]};
+    const double det = det3_cols(c0, c1, c2);
+    const int64_t gid = e * n3 + node;
+    if (det <= 0.0 || det != det) {
+      atomic_min_i64(first_bad, gid);
+      continue;
+    }
+    double inv[3][3];
+    inv[0][0] = (jac[1][1] * jac[2][2] - jac[1][2] * jac[2][1]) / det;
+    inv[0][1] = (jac[0][2] * jac[2][1] - jac[0][1] * jac[2][2]) / det;
+    inv[0][2] = (jac[0][1] * jac[1][2] - jac[0][2] * jac[1][1]) / det;
+    inv[1][0] = (jac[1][2] * jac[2][0] - jac[1][0] * jac[2][2]) / det;
+    inv[1][1] = (jac[0][0] * jac[2][2] - jac[0][2] * jac[2][0]) / det;
+    inv[1][2] = (jac[0][2] * jac[1][0] - jac[0][0] * jac[1][2]) / det;
+    inv[2][0] = (jac[1][0] * jac[2][1] - jac[1][1] * jac[2][0]) / det;
+    inv[2][1] = (jac[0][1] * jac[2][0] - jac[0][0] * jac[2][1]) / det;
+    inv[2][2] = (jac[0][0] * jac[1][1] - jac[0][1] * jac[1][0]) / det;
+    double m[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        m[a][c] = inv[a][0] * inv[c][0] + inv[a][1] * inv[c][1] + inv[a][2] * inv[c][2];
+    const double w = c_W[op + k] * c_W[op + j] * c_W[op + i];
+    const double scale = w * det;
+    double* g = g_out + e * 6 * n3 + node;
+    g[0 * n3] = scale * m[0][0];
+    g[1 * n3] = scale * m[0][1];
+    g[2 * n3] = scale * m[0][2];
+    g[3 * n3] = scale * m[1][1];
+    g[4 * n3] = scale * m[1][2];
+    g[5 * n3] = scale * m[2][2];
+    if (gwj_out) gwj_out[gid] = scale;
+  }
+}
+
 __device__ __forceinline__ double ppd_defect(const double* v, double& scale) {
   double d = 0.0, mx = 0.0;
   for (int c = 0; c < 3; ++c) {
@@ -248,6 +328,10 @@ extern "C" cudaError_t hx_setup_stored_impl(int n1, int64_t E, const double* ver
     if (e != cudaSuccess) return e;
   }
   // grid.x <= 2^31-1 elements
+  if (E > 0 && n1 == 8 && !std::getenv("HX_SETUP_GENERIC")) {
+    hx::stored_setup_kernel_ct<8><<<(unsigned)E, 256, 0, s>>>(E, verts, g, gwj, first_bad);
+    return cudaGetLastError();
+  }
   if (E > 0) hx::stored_setup_kernel<<<(unsigned)E, n3 < 256 ? n3 : 256, smem, s>>>(n1, E, verts, g, gwj, first_bad);
   return cudaGetLastError();
 }
