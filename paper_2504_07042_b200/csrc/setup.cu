@@ -52,6 +52,53 @@ __global__ void trilinear_setup_kernel(int n1, int64_t E, const double* __restri
   }
 }
 
+// The same at a compile-time order, one thread per k-fibre (element, i, j): the
+// vertices are loaded and the (i, j) pencil built once for the fibre's n1 nodes
+// instead of once per node (the per-node kernel reloads 24 vertex doubles and
+// divides 64-bit indices at every node). Same per-node arithmetic.
+template <int N1T>
+__global__ void __launch_bounds__(256) trilinear_setup_fibre_kernel(int64_t E, const double* __restrict__ verts,
+                                                                    int mode, int64_t* first_bad, double* out_a,
+                                                                    double* out_b, const double* __restrict__ lam0,
+                                                                    double l0v, const double* __restrict__ lam1,
+                                                                    double l1v) {
+  constexpr int n1 = N1T, n2 = n1 * n1, n3 = n2 * n1;
+  const int64_t fid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (fid >= E * n2) return;
+  const int64_t e = fid / n2;
+  const int f = (int)(fid - e * n2), i = f % n1, j = f / n1;
+  const int op = off_p(n1);
+  double v[24];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(verts + e * 24) + q);
+    v[2 * q] = t.x;
+    v[2 * q + 1] = t.y;
+  }
+  TrilinearPencil p;
+  trilinear_pencil(v, c_X[op + i], c_X[op + j], p);
+#pragma unroll 1
+  for (int k = 0; k < n1; ++k) {
+    const int64_t gid = e * n3 + k * n2 + f;
+    double g[6], det;
+    trilinear_node(p, c_X[op + k], g, det);
+    if (det <= 0.0 || det != det) {
+      if (first_bad) atomic_min_i64(first_bad, gid);
+      continue;
+    }
+    if (mode == 0) continue;
+    const double w = c_W[op + k] * c_W[op + j] * c_W[op + i];
+    const double lam_geo = 0.125 * w / det;
+    if (mode == 1) {
+      out_a[gid] = lam_geo;
+    } else {
+      const double gwj_weighted = lam_geo * (0.015625 * det * det);
+      out_a[gid] = lam_geo * (lam0 ? lam0[gid] : l0v);
+      out_b[gid] = gwj_weighted * (lam1 ? lam1[gid] : l1v);
+    }
+  }
+}
+
 // Physical coordinate c of GLL node (i, j, k) under the trilinear map
 // (element_node_coords, mesh.py:130-137).
 __device__ __forceinline__ double node_coord(const double v[24], const double* xi, int i, int j, int k, int c) {
@@ -311,6 +358,12 @@ extern "C" cudaError_t hx_setup_trilinear_impl(int n1, int64_t E, const double* 
                                                double l0v, const double* lam1, double l1v, cudaStream_t s) {
   if (first_bad) hx::init_i64<<<1, 1, 0, s>>>(first_bad, INT64_MAX);
   const int64_t n = E * n1 * n1 * n1;
+  // 16-byte aligned vertices (double2 loads) at N = 7: one thread per k-fibre
+  if (n > 0 && n1 == 8 && (reinterpret_cast<uintptr_t>(verts) & 15) == 0 && !std::getenv("HX_SETUP_GENERIC")) {
+    hx::trilinear_setup_fibre_kernel<8><<<hx::grid_for(E * 64, 256), 256, 0, s>>>(E, verts, mode, first_bad, a, b,
+                                                                                 lam0, l0v, lam1, l1v);
+    return cudaGetLastError();
+  }
   if (n > 0)
     hx::trilinear_setup_kernel<<<hx::grid_for(n, 256), 256, 0, s>>>(n1, E, verts, mode, first_bad, a, b, lam0,
                                                                      l0v, lam1, l1v);
