@@ -491,3 +491,39 @@ def test_graphed_apply_matches_eager():
     replay()
     torch.cuda.synchronize()
     assert torch.equal(y, op.apply(x))
+
+
+def test_order7_setup_kernels_match_the_generic_order(monkeypatch):
+    """The N=7 setup kernels (stored factors at a compile-time order, trilinear
+    route one thread per k-fibre) produce bit for bit the generic-order
+    kernels' fields, and report the same first bad node."""
+    mesh = hx.box_mesh(9, 7, 5, 7, perturbation=0.15, seed=11)
+    verts = mesh.vertices_device(DEV)
+    E = verts.shape[0]
+    rng = np.random.default_rng(12)
+    l0 = torch.as_tensor(rng.uniform(0.5, 2.0, (E, 512)), device=DEV)
+    l1 = torch.as_tensor(rng.uniform(0.5, 2.0, (E, 512)), device=DEV)
+    basis = hx.SpectralBasis.build(7)
+
+    def fields():
+        st = hx.LocalOperator(hx.KernelSpec("helmholtz", 1, "stored", 7), verts, basis, lam0=1.1, lam1=0.4)
+        pa = hx.LocalOperator(hx.KernelSpec("poisson", 1, "trilinear-partial", 7), verts, basis)
+        me = hx.LocalOperator(hx.KernelSpec("helmholtz", 1, "trilinear-merged", 7), verts, basis, lam0=l0, lam1=l1)
+        return [st._g.clone(), st._gwj.clone(), pa._lam_geo.clone(), me._lam2.clone(), me._lam3.clone()]
+
+    def first_bad():
+        bad = mesh.vertices.copy()
+        bad[23] = bad[23][[1, 0, 3, 2, 5, 4, 7, 6]]
+        msgs = []
+        for src in ("trilinear", "stored"):
+            with pytest.raises(hx.GeometryError) as ex:
+                hx.LocalOperator(hx.KernelSpec("poisson", 1, src, 7), torch.as_tensor(bad, device=DEV), basis)
+            msgs.append(str(ex.value))
+        return msgs
+
+    fast, fast_bad = fields(), first_bad()
+    monkeypatch.setenv("HX_SETUP_GENERIC", "1")
+    generic, generic_bad = fields(), first_bad()
+    for a, b in zip(fast, generic):
+        assert torch.equal(a, b)
+    assert fast_bad == generic_bad
