@@ -358,7 +358,8 @@ extern "C" cudaError_t hx_setup_trilinear_impl(int n1, int64_t E, const double* 
                                                double l0v, const double* lam1, double l1v, cudaStream_t s) {
   if (first_bad) hx::init_i64<<<1, 1, 0, s>>>(first_bad, INT64_MAX);
   const int64_t n = E * n1 * n1 * n1;
-  // 16-byte aligned vertices (double2 loads) at N = 7: one thread per k-fibre
+  // 16-byte aligned vertices (double2 loads) at N = 7: one thread per k-fibre (bitwise
+  // the same results; HX_SETUP_GENERIC=1 forces the per-node kernel, A/B and tests only)
   if (n > 0 && n1 == 8 && (reinterpret_cast<uintptr_t>(verts) & 15) == 0 && !std::getenv("HX_SETUP_GENERIC")) {
     hx::trilinear_setup_fibre_kernel<8><<<hx::grid_for(E * 64, 256), 256, 0, s>>>(E, verts, mode, first_bad, a, b,
                                                                                  lam0, l0v, lam1, l1v);
@@ -380,7 +381,9 @@ extern "C" cudaError_t hx_setup_stored_impl(int n1, int64_t E, const double* ver
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  // grid.x <= 2^31-1 elements
+  // grid.x <= 2^31-1 elements. N = 7 takes the compile-time-order kernel (bitwise the
+  // same fields); HX_SETUP_GENERIC=1 forces the generic one (A/B and the GPU test
+  // test_order7_setup_kernels_match_the_generic_order only)
   if (E > 0 && n1 == 8 && !std::getenv("HX_SETUP_GENERIC")) {
     hx::stored_setup_kernel_ct<8><<<(unsigned)E, 256, 0, s>>>(E, verts, g, gwj, first_bad);
     return cudaGetLastError();
