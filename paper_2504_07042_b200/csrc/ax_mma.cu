@@ -343,7 +343,8 @@ struct Tri {
     double sc = tri_rdet<K>(f[b], dt);
     if (HELM) {
       const int n = K * 64 + L.g * 8 + 2 * L.q + b;
-      const double l0 = lam0 ? sf[n] : l0v, l1 = lam1 ? sf[N3 + n] : l1v;
+      const double l0 = lam0 ? (sf ? sf[n] : __ldg(lam0 + n)) : l0v;
+      const double l1 = lam1 ? (sf ? sf[N3 + n] : __ldg(lam1 + n)) : l1v;
       v[7] = l1 * (dt * cm[b]);
       sc = l0 * sc;
     }
@@ -413,8 +414,8 @@ struct TriStoredScale {
   __device__ __forceinline__ void node_factors(const ElemGeo& S, const Lane& L, int b, double v[kNF]) const {
     tri_adj<K>(f[b], S.t00[K][L.g], S.t11[K][2 * L.q + b], v);
     const int n = K * 64 + L.g * 8 + 2 * L.q + b;
-    v[6] = sf[n];
-    if (MERGED) v[7] = sf[N3 + n];
+    v[6] = sf ? sf[n] : __ldg(sa + n);
+    if (MERGED) v[7] = sf ? sf[N3 + n] : __ldg(sb + n);
   }
   __device__ __forceinline__ static void apply(const double v[kNF], double x0, double x1, double x2, double xk,
                                                double& rr, double& ss, double& tt, double& ms) {
@@ -906,6 +907,18 @@ ax8m(const __grid_constant__ hx_axlocal_args a) {
   }
 }
 
+// fields staged by ax8m3: none by default -- the factor phase reads them from
+// global memory, so the Helmholtz CTA fits 4 per SM instead of 3 (145 vs 121
+// GDOF/s same box, profiles/r02_mma3_xstage_ab.txt); HX_MMA3_STAGE stages them (A/B)
+template <typename F>
+constexpr int kStage3() {
+#ifdef HX_MMA3_STAGE
+  return F::kStage;
+#else
+  return 0;
+#endif
+}
+
 // n_col = 3 with factor reuse, trilinear sources: one CTA of three warps per
 // element, warp c owning column c.  Stage A by the whole CTA; then warps 0 / 1
 // prepare fibre b = 0 / 1 of their lanes and evaluate its per-node factors
@@ -916,7 +929,7 @@ ax8m(const __grid_constant__ hx_axlocal_args a) {
 template <typename F, int NREG>
 __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args a) {
   constexpr int MINB = 65536 / (32 * NREG);
-  constexpr int NS = F::kStage;
+  constexpr int NS = kStage3<F>();
   __shared__ ElemGeo S;
   __shared__ double s_tile[2][2][64];  // warps 1, 2 (warp 0 uses S.tile)
   __shared__ uint64_t bar[1];
@@ -973,7 +986,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
   __syncthreads();
   {
     F fac;
-    fac.sf = sf;
+    fac.sf = NS > 0 ? sf : nullptr;  // null: the factor phase reads the fields from global memory
 #ifdef HX_MMA3_FIBRE_SPLIT  // warps 0 / 1 one fibre each, all slices (A/B: -3 %)
     if (w < 2) {
       fac.prepare_one(a, S, L, w);
@@ -1048,7 +1061,7 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
 // dynamic shared memory of ax8m3<F>: factors (>= the y tile), x, staged fields
 template <typename F>
 constexpr size_t ax8m3_dsmem() {
-  return sizeof(double) * (2 * 8 * F::kNF * 32 + 3 * N3 + F::kStage * N3);
+  return sizeof(double) * (2 * 8 * F::kNF * 32 + 3 * N3 + kStage3<F>() * N3);
 }
 
 
