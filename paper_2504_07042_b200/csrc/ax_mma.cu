@@ -36,10 +36,20 @@
 // of the even-odd 48, and DMMA mixed with DFMA costs ~5.6 pipe cycles per DMMA
 // (profiles/r02_ubench_mix.txt); DESIGN.md §4.1a has the budget and the A/B.
 //
-// n_col = 3 runs one warp per (element, column) with the n_col = 1 code, so
-// n_col = 3 == 3 x n_col = 1 bitwise (test_axlocal.py:180-199); the factor reuse
-// across columns of ax8c3 is given up for that (a column loop makes NVVM hoist
-// the constant operands into registers and spill).
+// Per-node fields (Helmholtz lam0 / lam1, the stored scale of partial, lam2 /
+// lam3 of merged) reach the node stage through shared memory: one bulk copy
+// (cp.async.bulk + mbarrier) per array per element, issued before the geometry
+// prologue, so no registers hold them and no load latency sits in the slices.
+//
+// n_col = 3 (every column bitwise an n_col = 1 apply, test_axlocal.py:180-199):
+// one CTA of three warps per element, warp c on column c; the element's
+// interleaved x arrives by one bulk copy and y leaves through a shared tile as
+// contiguous 16-byte stores. Either each warp runs the n_col = 1 column pass
+// (ax8m with CTA3), or (ax8m3) warps 0 / 1 first evaluate the per-node factors
+// once into shared memory and every warp's column pass reads them back.
+//
+// Fused BP5 gather (every policy): x read straight from the slab lattice, the
+// CG direction update p = r + beta p optionally applied on the fly.
 #include "n7_common.cuh"
 #include <type_traits>
 
