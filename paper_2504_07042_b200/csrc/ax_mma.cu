@@ -663,6 +663,23 @@ __device__ __forceinline__ XS make_xs(const hx_axlocal_args& a, const Lane& L, i
     return XSrc<NCOL, GATHER, CGP>(a, L, col);
 }
 
+// The element's y from a column-major shared tile [3][512] to the interleaved
+// (512 x 3) rows in global memory: thread v takes nodes 2v, 2v+1, reads their
+// three columns (16-byte, conflict-free) and writes 48 contiguous bytes. (The
+// row-major tile written by the column warps had 4-way bank conflicts:
+// profiles/r02_ncu_mma_ncol3.txt.)
+__device__ __forceinline__ void store_y_tile3(const double* __restrict__ sy, double* __restrict__ y) {
+  for (int v = threadIdx.x; v < N3 / 2; v += 96) {
+    const double2 c0 = *reinterpret_cast<const double2*>(sy + 2 * v);
+    const double2 c1 = *reinterpret_cast<const double2*>(sy + N3 + 2 * v);
+    const double2 c2 = *reinterpret_cast<const double2*>(sy + 2 * N3 + 2 * v);
+    double2* d = reinterpret_cast<double2*>(y + 6 * v);
+    d[0] = make_double2(c0.x, c1.x);
+    d[1] = make_double2(c2.x, c0.y);
+    d[2] = make_double2(c1.y, c2.y);
+  }
+}
+
 // One column of one element: x -> y, with the geometry prepared.
 // The transposed r / s products of a slice, accumulated into (y0, y1) from
 // the mass term ms: one order for every kernel built from these templates
@@ -780,8 +797,7 @@ __device__ __forceinline__ void column(const hx_axlocal_args& a, ElemGeo& S, dou
       xa[k] = y0;
       xb[k] = y1;
     } else if constexpr (YO == YOut::kTile) {
-      ysh[n * NCOL + col] = y0;
-      ysh[(n + 1) * NCOL + col] = y1;
+      *reinterpret_cast<double2*>(ysh + col * N3 + n) = make_double2(y0, y1);  // column-major tile
     } else if constexpr (NCOL == 1) {
       *reinterpret_cast<double2*>(ye + n) = make_double2(y0, y1);
     } else {
@@ -911,9 +927,7 @@ ax8m(const __grid_constant__ hx_axlocal_args a) {
                                                         XST ? sxy + 3 * N3 : nullptr);
   if constexpr (XST) {  // the y tile out as contiguous 16-byte stores
     __syncthreads();
-    const double2* src = reinterpret_cast<const double2*>(sxy + 3 * N3);
-    double2* dst = reinterpret_cast<double2*>(a.y + L.e * 3 * N3);
-    for (int v = threadIdx.x; v < 3 * N3 / 2; v += 96) dst[v] = src[v];
+    store_y_tile3(sxy + 3 * N3, a.y + L.e * 3 * N3);
   }
 }
 
@@ -1059,13 +1073,10 @@ __global__ void __maxnreg__(NREG) ax8m3(const __grid_constant__ hx_axlocal_args 
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int n = k * 64 + L.g * 8 + 2 * L.q;
-    sy[n * 3 + w] = xa[k];
-    sy[(n + 1) * 3 + w] = xb[k];
+    *reinterpret_cast<double2*>(sy + w * N3 + n) = make_double2(xa[k], xb[k]);  // column-major
   }
   __syncthreads();
-  const double2* src = reinterpret_cast<const double2*>(sy);
-  double2* dst = reinterpret_cast<double2*>(a.y + L.e * 3 * N3);
-  for (int v = threadIdx.x; v < 3 * N3 / 2; v += 96) dst[v] = src[v];
+  store_y_tile3(sy, a.y + L.e * 3 * N3);
 }
 
 // dynamic shared memory of ax8m3<F>: factors (>= the y tile), x, staged fields
