@@ -1137,8 +1137,10 @@ extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
   if (a->order != 7) return cudaErrorNotSupported;
   if (((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->y)) & (a->gather ? 7u : 15u)) != 0)
     return cudaErrorNotSupported;
-  // per-node fields: double2 loads and 16-byte bulk copies
-  const uintptr_t fields = reinterpret_cast<uintptr_t>(a->lam0) | reinterpret_cast<uintptr_t>(a->lam1) |
+  // per-node fields: double2 loads and 16-byte bulk copies; vertices: the 16-byte
+  // aligned L2 bulk prefetch
+  const uintptr_t fields = reinterpret_cast<uintptr_t>(a->verts) |
+                           reinterpret_cast<uintptr_t>(a->lam0) | reinterpret_cast<uintptr_t>(a->lam1) |
                            reinterpret_cast<uintptr_t>(a->lam2) | reinterpret_cast<uintptr_t>(a->lam3) |
                            reinterpret_cast<uintptr_t>(a->lam_geo) | reinterpret_cast<uintptr_t>(a->g) |
                            reinterpret_cast<uintptr_t>(a->gwj);
