@@ -376,9 +376,13 @@ def hx_arm(args, world):
     import paper_2504_07042_b200 as hx
     from paper_2504_07042_b200.workload import workload_count
 
-    dev = torch.device("cuda", world.local_rank)
+    # HX_BENCH_PLUMBING=1: N ranks on fewer GPUs over gloo -- runs the multi-rank code
+    # path (slabs, barriers, max-over-ranks, clock gather, e2e) where only one GPU
+    # exists; a plumbing check, never a measurement (marked in the JSON line)
+    plumbing = os.environ.get("HX_BENCH_PLUMBING") == "1" and world.size > 1
+    dev = torch.device("cuda", world.local_rank % torch.cuda.device_count() if plumbing else world.local_rank)
     torch.cuda.set_device(dev)
-    world.init("nccl")
+    world.init("gloo" if plumbing else "nccl")
     ex, ey, ez = MESH if args.mesh is None else tuple(int(v) for v in args.mesh.split(","))
     mesh = hx.box_mesh(ex, ey, ez, ORDER, perturbation=PERT, seed=SEED)
     z0, z1 = slab(world, ez)
@@ -452,6 +456,8 @@ def hx_arm(args, world):
             "hbm_peak_source": hbm_src,
         },
         "gpu_launches": args.steps,
+        **({"plumbing_check": True, "note": "N ranks on fewer GPUs over gloo: code-path check, not a measurement"}
+           if plumbing else {}),
         "clocks": main.get("clocks"),
     }
     if not args.no_variants:
