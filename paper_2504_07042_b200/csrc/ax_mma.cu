@@ -1149,9 +1149,12 @@ extern "C" cudaError_t hx_mma_launch(const hx_axlocal_args* a, cudaStream_t s) {
   switch (a->factor_source) {
     case HX_TRILINEAR:
       if (helm) {
-        // 232 registers: +1.5 % with coefficient fields, -0.7 % with scalars; 184 / 200: -6 / -2 %
-        // (after the field staging; profiles/r02_mma_fields_ab.txt for the numbers before it)
+        // coefficient fields: 232 registers (8 warps / SM), +1.5 %; scalars: 168 (232: -0.7 %);
+        // 184 / 200: -6 / -2 %. The register budget does not change the rounding (explicit
+        // fma, -fmad=false), so n_col = 1 stays bitwise the ax8m3 n_col = 3 columns.
+        // Hooks: 65 forces 232, 66 forces 168 (A/B)
         if (a->reserved == 65) return launch<Tri<true>, 232>(*a, s);
+        if (a->reserved != 66 && (a->lam0 || a->lam1)) return launch<Tri<true>, 232>(*a, s);
         return launch<Tri<true>>(*a, s);
       }
       switch (a->reserved) {  // register-cap A/B (tools/kernel_ab.py)
